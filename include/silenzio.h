@@ -1,0 +1,164 @@
+/*
+ * silenzio.h -- C ABI of the B200-native batched TFHE PBS library that runs the
+ * data-parallel hot path of Silenzio (arXiv 2504.17785).
+ *
+ * The paper evaluates every non-linear step of its integer training circuit as
+ * a TFHE programmable-bootstrapping table lookup (§II-C1 l.101 "TFHE's
+ * programmable bootstrapping (PBS)"; §III-D l.257 lookupComp /
+ * multivariateLookupComp) on integers of at most 8 bits, plus linear
+ * add/sub/scalar-mul (l.101). The paper contains no TFHE internals (it cites
+ * CGGI, l.48); the conventions used here are SURVEY.md §8(c) C1-C8 and are
+ * listed as readings R1-R21 in DESIGN.md.
+ *
+ * Conventions for every entry point:
+ *  - All array pointers are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *    unless the name ends in _host. The caller owns all memory; the library
+ *    allocates nothing and keeps no per-call state. The only process-wide
+ *    state is a read-only table of FFT twiddles, built once per device.
+ *  - Torus elements are uint64_t (q = 2^64, wrapping). LWE ciphertexts are
+ *    mask-then-body, row-major: [count][dim+1].
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *    All calls are stream-ordered and asynchronous; kernel faults surface at
+ *    the caller's next synchronisation.
+ *  - Return 0 (SILENZIO_OK) or a negative silenzio_status. No exceptions cross
+ *    the ABI. No CPU fallback exists: if a shape is not supported by a kernel,
+ *    SILENZIO_ERR_UNSUPPORTED is returned and nothing is launched.
+ *  - Deterministic: same inputs give bit-identical outputs (fixed reduction
+ *    order, no floating-point atomics).
+ */
+#ifndef SILENZIO_H
+#define SILENZIO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  uint32_t lwe_dim;      /* n, small-key LWE dimension            742 | 900 | 1024 */
+  uint32_t glwe_dim;     /* k (only k = 1 is supported)           1 */
+  uint32_t poly_size;    /* N, power of two                       2048 | 8192 | 32768 */
+  uint32_t pbs_base_log; /* log2 B_pbs                            23 | 15 | 15 */
+  uint32_t pbs_level;    /* l                                     1 | 2 | 2 */
+  uint32_t ks_base_log;  /* log2 B_ks                             3 | 4 | 4 */
+  uint32_t ks_level;     /* l_ks                                  5 | 4 | 5 */
+  uint32_t ks_in_dim;    /* KS input dimension (k*N of the producing set) */
+  uint32_t fft_limbs;    /* P in {1,2,3}: signed limbs per Fourier BSK coefficient */
+  uint32_t limb_bits;    /* width of the low limbs; the top limb takes 64-(P-1)*limb_bits */
+} silenzio_params;
+
+typedef enum {
+  SILENZIO_OK = 0,
+  SILENZIO_ERR_INVALID_PARAM = -1, /* inconsistent or out-of-range parameter */
+  SILENZIO_ERR_UNSUPPORTED = -2,   /* valid TFHE parameters no kernel implements */
+  SILENZIO_ERR_NULL_POINTER = -3,
+  SILENZIO_ERR_MISALIGNED = -4,    /* pointer not 16-byte aligned */
+  SILENZIO_ERR_COUNT = -5,         /* count = 0 where not allowed, or overflow */
+  SILENZIO_ERR_WINDOW = -6,        /* gadget driver: value window larger than a PBS can evaluate */
+  SILENZIO_ERR_CUDA = -7,          /* a CUDA launch / runtime call failed */
+  SILENZIO_ERR_WORKSPACE = -8      /* workspace missing or too small */
+} silenzio_status;
+
+const char *silenzio_status_string(int status);
+/* Library version string (build id). */
+const char *silenzio_version(void);
+
+/* ---------------------------------------------------------------- sizing */
+/* Bytes of the Fourier-domain bootstrapping key: n*(k+1)l*(k+1)*P*(N/2)*16. */
+size_t silenzio_fourier_bsk_bytes(const silenzio_params *params);
+/* Bytes of workspace silenzio_pbs_batch needs for `count` ciphertexts
+ * (the keyswitched small-key LWEs, count*(n+1)*8, rounded up). */
+size_t silenzio_pbs_workspace_bytes(const silenzio_params *params, size_t count);
+
+/* ------------------------------------------------------- hot-path calls */
+/* BSK -> Fourier (offline, once per key).
+ *  bsk          [n][(k+1)l][k+1][N] u64, standard domain (GGSW of s_i, C6).
+ *  fourier_bsk  opaque, silenzio_fourier_bsk_bytes() bytes: each coefficient is
+ *               lifted to a signed integer, split into P signed limbs, folded
+ *               with the negacyclic twist and transformed with the same f64 FFT
+ *               the blind rotation uses, pre-scaled by 2/N. Layout is tiled to
+ *               the blind-rotation thread mapping (not user-visible). */
+int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fourier_bsk,
+                            const silenzio_params *params, void *stream);
+
+/* LWE keyswitch big key -> small key.
+ *  lwe_in  [count][ks_in_dim+1], ksk [ks_in_dim][l_ks][n+1], lwe_out [count][n+1].
+ *  out = (0,...,0,b) - sum_j sum_t Dec_t(a_j) * KSK[j][t], exact mod 2^64. */
+int silenzio_keyswitch_batch(const uint64_t *lwe_in, const uint64_t *ksk, uint64_t *lwe_out,
+                             size_t count, const silenzio_params *params, void *stream);
+
+/* Programmable bootstrapping, atomic pattern KS -> MS -> BR -> SE
+ * (R1).
+ *  lwe_in      [count][kN+1] big-key LWE ciphertexts
+ *  lut_ids     [count] u32 index into luts (ids >= num_luts are clamped to 0);
+ *              may be NULL (all ciphertexts use luts[0])
+ *  luts        [num_luts][N] test polynomials (silenzio_build_testpoly)
+ *  fourier_bsk from silenzio_bsk_to_fourier; ksk as in silenzio_keyswitch_batch
+ *  lwe_out     [count][kN+1] big-key LWE ciphertexts of LUT(message)
+ *  workspace   >= silenzio_pbs_workspace_bytes(params, count) device bytes.
+ * lwe_in and lwe_out must not alias. */
+int silenzio_pbs_batch(const uint64_t *lwe_in, const uint32_t *lut_ids, const uint64_t *luts,
+                       uint32_t num_luts, const void *fourier_bsk, const uint64_t *ksk,
+                       uint64_t *lwe_out, size_t count, const silenzio_params *params,
+                       void *workspace, void *stream);
+
+/* Blind rotation + sample extraction only (MS -> BR -> SE) of small-key
+ * inputs [count][n+1]; output [count][kN+1]. Used to check the stages
+ * separately against the oracle and for the literal MS->BR->SE->KS order. */
+int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_ids,
+                                const uint64_t *luts, uint32_t num_luts, const void *fourier_bsk,
+                                uint64_t *lwe_out, size_t count, const silenzio_params *params,
+                                void *stream);
+
+/* Same as silenzio_pbs_batch but lwe_in / lwe_out are HOST buffers (pinned
+ * memory recommended). Copies are chunked (`chunk` ciphertexts, 0 = auto) and
+ * overlapped with compute on two internal streams created per call; the call
+ * returns after the last output chunk has landed in host memory (synchronous).
+ * workspace must hold silenzio_pbs_host_workspace_bytes(params, chunk). */
+size_t silenzio_pbs_host_workspace_bytes(const silenzio_params *params, size_t chunk);
+int silenzio_pbs_batch_host(const uint64_t *lwe_in_host, const uint32_t *lut_ids_host,
+                            const uint64_t *luts, uint32_t num_luts, const void *fourier_bsk,
+                            const uint64_t *ksk, uint64_t *lwe_out_host, size_t count,
+                            size_t chunk, const silenzio_params *params, void *workspace);
+
+/* Linear LWE combination (PAPER.md l.101 linear ops):
+ *  out[i] = sum_{t<terms} coef[i][t] * in[idx[i][t]] + (0,...,0,cst[i])  mod 2^64.
+ *  in [*][dim+1], idx [count][terms] u32, coef [count][terms] i64,
+ *  cst [count] u64 (may be NULL), out [count][dim+1]; out must not alias in. */
+int silenzio_lwe_linear_batch(const uint64_t *in, const uint32_t *idx, const int64_t *coef,
+                              const uint64_t *cst, uint32_t terms, uint32_t dim, size_t count,
+                              uint64_t *out, void *stream);
+
+/* Test polynomial of a LUT:
+ *  v' = sum_{j<N} T[floor(j/box)] X^j, box = N / 2^p;  v = X^{-box/2} * v'.
+ *  tables [num][2^p] u64 torus values, polys [num][N] u64. */
+int silenzio_build_testpoly(const uint64_t *tables, uint32_t num, uint32_t p, uint32_t N,
+                            uint64_t *polys, void *stream);
+
+/* ------------------------------------- client-side key / ciphertext generation
+ * All random numbers are inputs (drawn by the caller), so every key and
+ * ciphertext is a deterministic function of the caller's seeded draws. */
+/* out[c] = (mask[c], <mask[c], key> + noise[c] + plaintext[c])  (C2). */
+int silenzio_lwe_encrypt_batch(const uint64_t *mask, const int64_t *noise,
+                               const uint64_t *plaintext, const uint64_t *key, uint32_t dim,
+                               size_t count, uint64_t *out, void *stream);
+/* phase[c] = b - <a, key>  (C2). */
+int silenzio_lwe_phase_batch(const uint64_t *ct, const uint64_t *key, uint32_t dim, size_t count,
+                             uint64_t *phase, void *stream);
+/* GGSW bootstrapping key (C6): mask [n][(k+1)l][k][N], noise [n][(k+1)l][N],
+ * lwe_key [n] in {0,1}, glwe_key [k][N] in {0,1} -> bsk [n][(k+1)l][k+1][N]. */
+int silenzio_bsk_generate(const uint64_t *lwe_key, const uint64_t *glwe_key, const uint64_t *mask,
+                          const int64_t *noise, uint64_t *bsk, const silenzio_params *params,
+                          void *stream);
+/* Keyswitching key (C3): KSK[j][t] = LWE_s(s_in[j] * 2^{64 - t*base_log}),
+ * mask [in_dim][level][n], noise [in_dim][level] -> ksk [in_dim][level][n+1]. */
+int silenzio_ksk_generate(const uint64_t *in_key, const uint64_t *lwe_key, const uint64_t *mask,
+                          const int64_t *noise, uint64_t *ksk, uint32_t in_dim, uint32_t n,
+                          uint32_t base_log, uint32_t level, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SILENZIO_H */

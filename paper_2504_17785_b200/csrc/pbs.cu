@@ -1,0 +1,411 @@
+// pbs.cu -- blind rotation (MS + ACC init + n x CMux + SE) and BSK -> Fourier
+// for k = 1, N = 2048 on sm_100a.
+//
+// Steps (conventions §8(c) C4-C7, R3-R6):
+//   MS:   a~_i = round(a_i * 2N / 2^64)                                  (a2)
+//   init: ACC = (0, X^{-b~} v)                                           (a3)
+//   CMux: ACC += ExtProd(BSK_i, X^{a~_i} ACC - ACC)   for i < n          (a4)
+//         rotate-diff -> signed digits -> forward FFT -> pointwise MAC with
+//         the Fourier BSK (P limbs) -> inverse FFT -> exact rounding and
+//         limb recombination mod 2^64 -> ACC +=
+//   SE:   coefficient 0 of ACC as a big-key LWE                          (a5)
+//
+// Design: persistent CTAs of 128 threads = two teams of
+// 64; team g owns GLWE component g (mask / body). ACC (2 x 2048 u64) stays in
+// shared memory for the whole CMux loop; the decomposed digits' spectra are
+// staged in shared memory (one 16 KiB array per GGSW row); every transform is
+// register resident (16 complex per thread) with two shared-memory exchanges.
+// The BSK is streamed from L2 (it is read once per CMux per ciphertext and is
+// laid out so each warp load is 512 contiguous bytes).
+#include <cmath>
+#include <mutex>
+
+#include "fft.cuh"
+
+namespace sz {
+
+__device__ Tables g_tables;
+
+static std::once_flag g_tables_once[64];
+static int g_tables_status[64];
+
+// Build the twiddle tables on the host in long double and round once to double.
+static int init_tables_for_device(int dev) {
+  Tables h;
+  const long double PI = 3.141592653589793238462643383279502884L;
+  for (int k = 0; k < 16; k++)
+    for (int t = 0; t < 64; t++) {
+      long double ang = PI * (long double)(t * (4 * k + 1)) / 2048.0L;
+      h.tw1[k * 64 + t] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+  for (int k = 0; k < 16; k++)
+    for (int s = 0; s < 4; s++) {
+      long double ang = 2.0L * PI * (long double)(s * k) / 64.0L;
+      h.tw2[k * 4 + s] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+  for (int m = 0; m < 16; m++) {
+    long double ang = PI * (long double)m / 32.0L;
+    h.twist[m] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  if (prev != dev && cudaSetDevice(dev) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  cudaError_t e = cudaMemcpyToSymbol(g_tables, &h, sizeof(Tables));
+  if (prev != dev) cudaSetDevice(prev);
+  return e == cudaSuccess ? SILENZIO_OK : SILENZIO_ERR_CUDA;
+}
+
+int ensure_tables() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SILENZIO_ERR_CUDA;
+  std::call_once(g_tables_once[dev], [dev] { g_tables_status[dev] = init_tables_for_device(dev); });
+  return g_tables_status[dev];
+}
+
+// ------------------------------------------------------------------ team FFT
+__device__ __forceinline__ void team_sync(int team) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(kTeam) : "memory");
+}
+
+// Forward transform. In: x[m] = folded value at j = t + 64 m (natural m).
+// Out: x[4u + r] = spectrum at position 4 (t + 64 u) + bitrev2(r) ("slot" order).
+__device__ __forceinline__ void fwd_fft(double2 (&x)[16], double2 *buf, int t, int team) {
+  const Tables &T = g_tables;
+  // negacyclic twist, part 1: w^{64 m} (the w^t part is folded into tw1)
+#pragma unroll
+  for (int m = 0; m < 16; m++) x[m] = cmul(x[m], T.twist[m]);
+  // pass 1: radix 16 over stride 64 (thread owns offset s = t)
+  dft<16, false>(x);
+  team_sync(team);
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int k = bitrev4(r);
+    const double2 w = __ldg(&T.tw1[k * 64 + t]);
+    buf[swz(t + 64 * k)] = cmul(x[r], w);
+  }
+  team_sync(team);
+  // pass 2: radix 16 over stride 4 inside blocks of 64
+  const int b = t >> 2, s = t & 3;
+  double2 y[16];
+#pragma unroll
+  for (int m = 0; m < 16; m++) y[m] = buf[swz(64 * b + s + 4 * m)];
+  dft<16, false>(y);
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int k = bitrev4(r);
+    const double2 w = __ldg(&T.tw2[k * 4 + s]);
+    buf[swz(64 * b + s + 4 * k)] = (k == 0) ? y[r] : cmul(y[r], w);
+  }
+  team_sync(team);
+  // pass 3: radix 4 over stride 1, four groups per thread
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    double2 z[4];
+#pragma unroll
+    for (int m = 0; m < 4; m++) z[m] = buf[swz(4 * (t + 64 * u) + m)];
+    dft<4, false>(z);
+#pragma unroll
+    for (int r = 0; r < 4; r++) x[4 * u + r] = z[r];
+  }
+}
+
+// Inverse transform (unnormalised). In: slot order as produced by fwd_fft.
+// Out: x[m] = value at j = t + 64 m, untwisted: (c_j + i c_{j+1024}) * M.
+__device__ __forceinline__ void inv_fft(double2 (&x)[16], double2 *buf, int t, int team) {
+  const Tables &T = g_tables;
+  team_sync(team);  // previous users of buf are done
+  // pass 3^-1
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    double2 z[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) z[k] = x[4 * u + bitrev2(k)];
+    dft<4, true>(z);
+#pragma unroll
+    for (int q = 0; q < 4; q++) buf[swz(4 * (t + 64 * u) + bitrev2(q))] = z[q];
+  }
+  team_sync(team);
+  // pass 2^-1
+  const int b = t >> 2, s = t & 3;
+  double2 y[16];
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    const double2 v = buf[swz(64 * b + s + 4 * k)];
+    y[k] = (k == 0) ? v : cmulc(v, __ldg(&T.tw2[k * 4 + s]));
+  }
+  dft<16, true>(y);
+#pragma unroll
+  for (int q = 0; q < 16; q++) buf[swz(64 * b + s + 4 * bitrev4(q))] = y[q];
+  team_sync(team);
+  // pass 1^-1
+#pragma unroll
+  for (int k = 0; k < 16; k++) x[k] = cmulc(buf[swz(t + 64 * k)], __ldg(&T.tw1[k * 64 + t]));
+  dft<16, true>(x);
+  // x[q] now holds m = bitrev4(q); reorder to natural m and untwist
+  double2 o[16];
+#pragma unroll
+  for (int q = 0; q < 16; q++) o[bitrev4(q)] = x[q];
+#pragma unroll
+  for (int m = 0; m < 16; m++) x[m] = cmulc(o[m], T.twist[m]);
+}
+
+// ------------------------------------------------------------- limb helpers
+__device__ __forceinline__ i64 sext(i64 x, int bits) {
+  return (bits >= 64) ? x : (i64)((u64)x << (64 - bits)) >> (64 - bits);
+}
+
+// Split a u64 torus coefficient into P signed limbs, limb p weighted 2^{p*w};
+// the top limb is reduced mod 2^{64-(P-1)w} (its weight makes higher bits vanish).
+__device__ __forceinline__ void limb_split(u64 g, int P, int w, double (&l)[3]) {
+  if (P == 1) {
+    l[0] = (double)(i64)g;
+    return;
+  }
+  const i64 l0 = sext((i64)g, w);
+  const u64 rem = (g - (u64)l0) >> w;  // exact: g - l0 = 0 mod 2^w
+  l[0] = (double)l0;
+  if (P == 2) {
+    l[1] = (double)sext((i64)rem, 64 - w);
+    return;
+  }
+  const i64 l1 = sext((i64)rem, w);
+  const i64 rem2 = ((i64)rem - l1) >> w;
+  l[1] = (double)l1;
+  l[2] = (double)sext(rem2, 64 - 2 * w);
+}
+
+// double (integer-valued up to rounding) -> round to nearest, mod 2^64
+__device__ __forceinline__ u64 f64_to_torus(double x) {
+  const double hi = floor(x * 0x1p-32);
+  const double lo = fma(hi, -0x1p32, x);  // exact
+  return ((u64)__double2ll_rn(hi) << 32) + (u64)__double2ll_rn(lo);
+}
+
+// x mod 2^bits for an integer-valued double |x| < 2^53 (exact)
+__device__ __forceinline__ double fmod_pow2(double x, double two_bits, double inv_two_bits) {
+  return fma(-floor(x * inv_two_bits), two_bits, x);
+}
+
+// ------------------------------------------------------------ BR kernel
+struct BRArgs {
+  const u64 *lwe_small;  // [count][n+1]
+  const u32 *lut_ids;    // [count] or null
+  const u64 *luts;       // [num_luts][N]
+  u32 num_luts;
+  const double2 *fbsk;   // [n][2][rows][P][16][64]
+  u64 *lwe_out;          // [count][N+1]
+  long count;
+  int n, level, base_log, P, w;
+};
+
+constexpr int kN = 2048;
+constexpr int kLog2_2N = 12;
+
+__host__ __device__ constexpr size_t br_smem_bytes(int rows, int n) {
+  return 2 * kN * sizeof(u64)                     // ACC
+         + (size_t)rows * kM * sizeof(double2)    // digit spectra
+         + 2 * kM * sizeof(double2)               // per-team exchange buffers
+         + ((size_t)n * sizeof(unsigned short) + 15) / 16 * 16;  // modswitched masks
+}
+
+__global__ void __launch_bounds__(128, 2) blind_rotate_kernel(BRArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int rows = 2 * A.level;
+  u64 *acc = reinterpret_cast<u64 *>(smem);                                  // [2][2048]
+  double2 *dsm = reinterpret_cast<double2 *>(smem + 2 * kN * sizeof(u64));  // [rows][16][64]
+  double2 *xbuf = dsm + (size_t)rows * kM;                                   // [2][1024]
+  unsigned short *abar = reinterpret_cast<unsigned short *>(xbuf + 2 * kM);
+
+  const int tid = threadIdx.x;
+  const int team = tid >> 6, t = tid & 63;
+  double2 *buf = xbuf + team * kM;
+  const int n = A.n, P = A.P, w = A.w;
+  const double two_w = ldexp(1.0, w);
+  const int top_bits = 64 - (P - 1) * w;
+  const double two_top = ldexp(1.0, top_bits), inv_two_top = ldexp(1.0, -top_bits);
+
+  for (long c = blockIdx.x; c < A.count; c += gridDim.x) {
+    const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
+    // ---- modulus switch (a2)
+    for (int i = tid; i < n; i += blockDim.x) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2N);
+    const int bt = (int)sz_modswitch(lwe[n], kLog2_2N);
+    // ---- ACC init (a3): ACC = (0, X^{-b~} v), (X^{-b} v)[j] = v[j + b] (negacyclic)
+    u32 id = A.lut_ids ? A.lut_ids[c] : 0u;
+    if (id >= A.num_luts) id = 0;
+    const u64 *v = A.luts + (size_t)id * kN;
+    for (int j = tid; j < kN; j += blockDim.x) {
+      acc[j] = 0;
+      const int idx = (j + bt) & (2 * kN - 1);
+      acc[kN + j] = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
+    }
+    __syncthreads();
+
+    for (int i = 0; i < n; i++) {
+      const int a = abar[i];
+      // ---------------- forward: digits of X^a ACC_g - ACC_g, one FFT per level
+      const u64 *accg = acc + team * kN;
+      for (int lvl = 1; lvl <= A.level; lvl++) {
+        double2 x[16];
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+          double dv[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int j = t + 64 * m + 1024 * h;
+            const int src = (j - a) & (2 * kN - 1);
+            const u64 rot = (src < kN) ? accg[src] : (u64)0 - accg[src - kN];
+            u64 r = sz_decomp_round(rot - accg[j], A.base_log, A.level);
+            i64 d = 0;
+            // peel digits t = l, l-1, ..., lvl  (level lvl has weight q/B^lvl)
+            for (int tt = A.level; tt >= lvl; tt--) d = sz_decomp_next(r, A.base_log);
+            dv[h] = (double)d;
+          }
+          x[m] = make_double2(dv[0], dv[1]);
+        }
+        fwd_fft(x, buf, t, team);
+        double2 *drow = dsm + (size_t)(team * A.level + (lvl - 1)) * kM;
+#pragma unroll
+        for (int sl = 0; sl < 16; sl++) drow[sl * 64 + t] = x[sl];
+      }
+      __syncthreads();
+      // ---------------- inverse: output component o = team, limbs top -> 0
+      const int o = team;
+      double2 V[16];
+      u64 *acco = acc + o * kN;
+      const double2 *Gi = A.fbsk + (size_t)i * 2 * rows * P * kM + (size_t)o * rows * P * kM;
+      for (int p = P - 1; p >= 0; p--) {
+        double2 y[16];
+#pragma unroll
+        for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
+        for (int row = 0; row < rows; row++) {
+          const double2 *G = Gi + ((size_t)row * P + p) * kM;
+          const double2 *D = dsm + (size_t)row * kM;
+#pragma unroll
+          for (int sl = 0; sl < 16; sl++) cmac(y[sl], D[sl * 64 + t], __ldg(&G[sl * 64 + t]));
+        }
+        inv_fft(y, buf, t, team);
+        // exact rounding + limb recombination (limb p has weight 2^{p w})
+        if (p == 0) {
+#pragma unroll
+          for (int m = 0; m < 16; m++) {
+            u64 lo = f64_to_torus(y[m].x), hi = f64_to_torus(y[m].y);
+            if (P > 1) {
+              lo += (u64)__double2ll_rn(V[m].x) << w;
+              hi += (u64)__double2ll_rn(V[m].y) << w;
+            }
+            acco[t + 64 * m] += lo;
+            acco[t + 64 * m + 1024] += hi;
+          }
+        } else if (p == P - 1) {
+#pragma unroll
+          for (int m = 0; m < 16; m++) {
+            V[m].x = fmod_pow2(rint(y[m].x), two_top, inv_two_top);
+            V[m].y = fmod_pow2(rint(y[m].y), two_top, inv_two_top);
+          }
+        } else {
+          const int bits = 64 - p * w;
+          const double tb = ldexp(1.0, bits), itb = ldexp(1.0, -bits);
+#pragma unroll
+          for (int m = 0; m < 16; m++) {
+            V[m].x = fmod_pow2(fma(V[m].x, two_w, rint(y[m].x)), tb, itb);
+            V[m].y = fmod_pow2(fma(V[m].y, two_w, rint(y[m].y)), tb, itb);
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // ---- sample extraction (a5)
+    u64 *out = A.lwe_out + (size_t)c * (kN + 1);
+    for (int j = tid; j <= kN; j += blockDim.x) {
+      u64 val;
+      if (j == 0) val = acc[0];
+      else if (j < kN) val = (u64)0 - acc[kN - j];
+      else val = acc[kN];
+      out[j] = val;
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------- BSK -> Fourier
+struct B2FArgs {
+  const u64 *bsk;  // [n][rows][2][N]
+  double2 *fbsk;   // [n][2][rows][P][16][64]
+  int n, rows, P, w;
+};
+
+// one team (64 threads) per (i, row, o, p)
+__global__ void __launch_bounds__(64) bsk_to_fourier_kernel(B2FArgs A) {
+  __shared__ __align__(16) double2 buf[kM];
+  const int t = threadIdx.x;
+  long blk = blockIdx.x;
+  const int p = blk % A.P; blk /= A.P;
+  const int o = blk % 2; blk /= 2;
+  const int row = blk % A.rows; blk /= A.rows;
+  const int i = (int)blk;
+  const u64 *g = A.bsk + (((size_t)i * A.rows + row) * 2 + o) * kN;
+  double2 x[16];
+#pragma unroll
+  for (int m = 0; m < 16; m++) {
+    double l0[3], l1[3];
+    limb_split(g[t + 64 * m], A.P, A.w, l0);
+    limb_split(g[t + 64 * m + 1024], A.P, A.w, l1);
+    x[m] = make_double2(l0[p], l1[p]);
+  }
+  fwd_fft(x, buf, t, 0);
+  double2 *dst = A.fbsk + ((((size_t)i * 2 + o) * A.rows + row) * A.P + p) * kM;
+  const double scale = 1.0 / kM;
+#pragma unroll
+  for (int sl = 0; sl < 16; sl++) dst[sl * 64 + t] = make_double2(x[sl].x * scale, x[sl].y * scale);
+}
+
+// ------------------------------------------------------------ host launch
+int launch_blind_rotate(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
+                        const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
+                        cudaStream_t stream) {
+  int st = ensure_tables();
+  if (st != SILENZIO_OK) return st;
+  BRArgs A;
+  A.lwe_small = lwe_small;
+  A.lut_ids = lut_ids;
+  A.luts = luts;
+  A.num_luts = num_luts;
+  A.fbsk = reinterpret_cast<const double2 *>(fbsk);
+  A.lwe_out = lwe_out;
+  A.count = (long)count;
+  A.n = (int)P->lwe_dim;
+  A.level = (int)P->pbs_level;
+  A.base_log = (int)P->pbs_base_log;
+  A.P = (int)P->fft_limbs;
+  A.w = (int)P->limb_bits;
+  const size_t smem = br_smem_bytes(2 * A.level, A.n);
+  SZ_CUDA_OK(cudaFuncSetAttribute(blind_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 0, per_sm = 0;
+  SZ_CUDA_OK(cudaGetDevice(&dev));
+  SZ_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SZ_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blind_rotate_kernel, 128, smem));
+  if (per_sm < 1) return SILENZIO_ERR_UNSUPPORTED;
+  const long resident = (long)sms * per_sm;
+  const long grid = (long)count < resident ? (long)count : resident;
+  blind_rotate_kernel<<<(unsigned)grid, 128, smem, stream>>>(A);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+int launch_bsk_to_fourier(const u64 *bsk, void *fbsk, const silenzio_params *P, cudaStream_t stream) {
+  int st = ensure_tables();
+  if (st != SILENZIO_OK) return st;
+  B2FArgs A;
+  A.bsk = bsk;
+  A.fbsk = reinterpret_cast<double2 *>(fbsk);
+  A.n = (int)P->lwe_dim;
+  A.rows = 2 * (int)P->pbs_level;
+  A.P = (int)P->fft_limbs;
+  A.w = (int)P->limb_bits;
+  const long blocks = (long)A.n * A.rows * 2 * A.P;
+  bsk_to_fourier_kernel<<<(unsigned)blocks, 64, 0, stream>>>(A);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+}  // namespace sz

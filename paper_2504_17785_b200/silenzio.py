@@ -1,0 +1,239 @@
+"""Thin ctypes binding of libsilenzio (include/silenzio.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA
+kernels of libsilenzio.so. Tensors are torch CUDA tensors (int64 storage is
+reinterpreted as u64 by the library); there is no CPU fallback -- if the
+library is missing or a call fails, an exception is raised.
+"""
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsilenzio.so")
+
+_lib = None
+
+
+class SilenzioError(RuntimeError):
+    pass
+
+
+class silenzio_params(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_uint32) for name in (
+        "lwe_dim", "glwe_dim", "poly_size", "pbs_base_log", "pbs_level",
+        "ks_base_log", "ks_level", "ks_in_dim", "fft_limbs", "limb_bits")]
+
+
+def load():
+    """Load libsilenzio.so (built in-tree by __graft_entry__.build())."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise SilenzioError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    V, P, S = ctypes.c_void_p, ctypes.POINTER(silenzio_params), ctypes.c_size_t
+    U32, I = ctypes.c_uint32, ctypes.c_int
+    sigs = {
+        "silenzio_status_string": ([I], ctypes.c_char_p),
+        "silenzio_version": ([], ctypes.c_char_p),
+        "silenzio_fourier_bsk_bytes": ([P], S),
+        "silenzio_pbs_workspace_bytes": ([P, S], S),
+        "silenzio_pbs_host_workspace_bytes": ([P, S], S),
+        "silenzio_bsk_to_fourier": ([V, V, P, V], I),
+        "silenzio_keyswitch_batch": ([V, V, V, S, P, V], I),
+        "silenzio_pbs_batch": ([V, V, V, U32, V, V, V, S, P, V, V], I),
+        "silenzio_blind_rotate_batch": ([V, V, V, U32, V, V, S, P, V], I),
+        "silenzio_pbs_batch_host": ([V, V, V, U32, V, V, V, S, S, P, V], I),
+        "silenzio_lwe_linear_batch": ([V, V, V, V, U32, U32, S, V, V], I),
+        "silenzio_build_testpoly": ([V, U32, U32, U32, V, V], I),
+        "silenzio_lwe_encrypt_batch": ([V, V, V, V, U32, S, V, V], I),
+        "silenzio_lwe_phase_batch": ([V, V, U32, S, V, V], I),
+        "silenzio_bsk_generate": ([V, V, V, V, V, P, V], I),
+        "silenzio_ksk_generate": ([V, V, V, V, V, U32, U32, U32, U32, V], I),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    return [
+        "silenzio_status_string", "silenzio_version", "silenzio_fourier_bsk_bytes",
+        "silenzio_pbs_workspace_bytes", "silenzio_pbs_host_workspace_bytes",
+        "silenzio_bsk_to_fourier", "silenzio_keyswitch_batch", "silenzio_pbs_batch",
+        "silenzio_blind_rotate_batch", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
+        "silenzio_build_testpoly", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
+        "silenzio_bsk_generate", "silenzio_ksk_generate",
+    ]
+
+
+def _check(rc):
+    if rc != 0:
+        msg = load().silenzio_status_string(rc).decode()
+        raise SilenzioError(f"libsilenzio error {rc}: {msg}")
+
+
+def make_params(P) -> silenzio_params:
+    """silenzio_params from any object with the synth.Params fields."""
+    return silenzio_params(P.n, P.k, P.N, P.pbs_base_log, P.pbs_level, P.ks_base_log,
+                           P.ks_level, getattr(P, "ks_in_dim", P.k * P.N), P.fft_limbs,
+                           P.limb_bits)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise SilenzioError("device tensor expected")
+    if not t.is_contiguous():
+        raise SilenzioError("contiguous tensor expected")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _hptr(t):
+    if t is None:
+        return None
+    if t.is_cuda or not t.is_contiguous():
+        raise SilenzioError("contiguous host tensor expected")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _u64_view(t):
+    # torch has no uint64 arithmetic we need; int64 storage is bit-identical
+    return t if t.dtype == torch.int64 else t.view(torch.int64)
+
+
+@dataclass
+class Params:
+    """ABI params mirror (fields of silenzio_params) built from synth.Params."""
+    raw: silenzio_params
+
+    @classmethod
+    def of(cls, P):
+        return cls(make_params(P))
+
+
+def fourier_bsk_bytes(P) -> int:
+    return load().silenzio_fourier_bsk_bytes(ctypes.byref(make_params(P)))
+
+
+def pbs_workspace_bytes(P, count: int) -> int:
+    return load().silenzio_pbs_workspace_bytes(ctypes.byref(make_params(P)), count)
+
+
+def pbs_host_workspace_bytes(P, chunk: int) -> int:
+    return load().silenzio_pbs_host_workspace_bytes(ctypes.byref(make_params(P)), chunk)
+
+
+def bsk_to_fourier(bsk, P, stream=None):
+    """bsk [n][(k+1)l][k+1][N] (int64 view of u64) -> opaque Fourier BSK (uint8 tensor)."""
+    nbytes = fourier_bsk_bytes(P)
+    out = torch.empty(nbytes, dtype=torch.uint8, device=bsk.device)
+    _check(load().silenzio_bsk_to_fourier(_ptr(bsk), _ptr(out), ctypes.byref(make_params(P)), _stream(stream)))
+    return out
+
+
+def keyswitch_batch(lwe_in, ksk, P, out=None, stream=None):
+    count = lwe_in.shape[0]
+    if out is None:
+        out = torch.empty((count, P.n + 1), dtype=torch.int64, device=lwe_in.device)
+    _check(load().silenzio_keyswitch_batch(_ptr(lwe_in), _ptr(ksk), _ptr(out), count,
+                                           ctypes.byref(make_params(P)), _stream(stream)))
+    return out
+
+
+def pbs_batch(lwe_in, lut_ids, luts, fourier_bsk, ksk, P, out=None, workspace=None, stream=None):
+    count = lwe_in.shape[0]
+    if out is None:
+        out = torch.empty((count, P.k * P.N + 1), dtype=torch.int64, device=lwe_in.device)
+    if workspace is None:
+        workspace = torch.empty(pbs_workspace_bytes(P, count), dtype=torch.uint8, device=lwe_in.device)
+    num_luts = luts.shape[0] if luts.dim() == 2 else 1
+    _check(load().silenzio_pbs_batch(_ptr(lwe_in), _ptr(lut_ids), _ptr(luts), num_luts, _ptr(fourier_bsk),
+                                     _ptr(ksk), _ptr(out), count, ctypes.byref(make_params(P)),
+                                     _ptr(workspace), _stream(stream)))
+    return out
+
+
+def blind_rotate_batch(lwe_small, lut_ids, luts, fourier_bsk, P, out=None, stream=None):
+    count = lwe_small.shape[0]
+    if out is None:
+        out = torch.empty((count, P.k * P.N + 1), dtype=torch.int64, device=lwe_small.device)
+    num_luts = luts.shape[0] if luts.dim() == 2 else 1
+    _check(load().silenzio_blind_rotate_batch(_ptr(lwe_small), _ptr(lut_ids), _ptr(luts), num_luts,
+                                              _ptr(fourier_bsk), _ptr(out), count,
+                                              ctypes.byref(make_params(P)), _stream(stream)))
+    return out
+
+
+def pbs_batch_host(lwe_in_host, lut_ids_host, luts, fourier_bsk, ksk, P, out_host, workspace, chunk=0):
+    """Host-buffer PBS (chunked H2D / compute / D2H overlap inside the library)."""
+    count = lwe_in_host.shape[0]
+    num_luts = luts.shape[0] if luts.dim() == 2 else 1
+    _check(load().silenzio_pbs_batch_host(_hptr(lwe_in_host), _hptr(lut_ids_host), _ptr(luts), num_luts,
+                                          _ptr(fourier_bsk), _ptr(ksk), _hptr(out_host), count, chunk,
+                                          ctypes.byref(make_params(P)), _ptr(workspace)))
+    return out_host
+
+
+def lwe_linear_batch(lwe_in, idx, coef, cst, out=None, stream=None):
+    count, terms = idx.shape
+    dim = lwe_in.shape[-1] - 1
+    if out is None:
+        out = torch.empty((count, dim + 1), dtype=torch.int64, device=lwe_in.device)
+    _check(load().silenzio_lwe_linear_batch(_ptr(lwe_in), _ptr(idx), _ptr(coef), _ptr(cst), terms, dim, count,
+                                            _ptr(out), _stream(stream)))
+    return out
+
+
+def build_testpoly(tables, p, N, stream=None):
+    num = tables.shape[0]
+    out = torch.empty((num, N), dtype=torch.int64, device=tables.device)
+    _check(load().silenzio_build_testpoly(_ptr(tables), num, p, N, _ptr(out), _stream(stream)))
+    return out
+
+
+def lwe_encrypt_batch(mask, noise, plaintext, key, out=None, stream=None):
+    count, dim = mask.shape
+    if out is None:
+        out = torch.empty((count, dim + 1), dtype=torch.int64, device=mask.device)
+    _check(load().silenzio_lwe_encrypt_batch(_ptr(mask), _ptr(noise), _ptr(plaintext), _ptr(key), dim, count,
+                                             _ptr(out), _stream(stream)))
+    return out
+
+
+def lwe_phase_batch(ct, key, out=None, stream=None):
+    count, dim1 = ct.shape
+    if out is None:
+        out = torch.empty(count, dtype=torch.int64, device=ct.device)
+    _check(load().silenzio_lwe_phase_batch(_ptr(ct), _ptr(key), dim1 - 1, count, _ptr(out), _stream(stream)))
+    return out
+
+
+def bsk_generate(lwe_key, glwe_key, mask, noise, P, stream=None):
+    rows = (P.k + 1) * P.pbs_level
+    out = torch.empty((P.n, rows, P.k + 1, P.N), dtype=torch.int64, device=mask.device)
+    _check(load().silenzio_bsk_generate(_ptr(lwe_key), _ptr(glwe_key), _ptr(mask), _ptr(noise), _ptr(out),
+                                        ctypes.byref(make_params(P)), _stream(stream)))
+    return out
+
+
+def ksk_generate(in_key, lwe_key, mask, noise, base_log, level, stream=None):
+    in_dim, lv, n = mask.shape
+    assert lv == level
+    out = torch.empty((in_dim, level, n + 1), dtype=torch.int64, device=mask.device)
+    _check(load().silenzio_ksk_generate(_ptr(in_key), _ptr(lwe_key), _ptr(mask), _ptr(noise), _ptr(out), in_dim, n,
+                                        base_log, level, _stream(stream)))
+    return out
