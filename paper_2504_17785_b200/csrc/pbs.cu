@@ -25,6 +25,7 @@
 namespace sz {
 
 __device__ Tables g_tables;
+__constant__ double2 c_twist[16];
 
 static std::once_flag g_tables_once[64];
 static int g_tables_status[64];
@@ -51,6 +52,7 @@ static int init_tables_for_device(int dev) {
   if (cudaGetDevice(&prev) != cudaSuccess) return SILENZIO_ERR_CUDA;
   if (prev != dev && cudaSetDevice(dev) != cudaSuccess) return SILENZIO_ERR_CUDA;
   cudaError_t e = cudaMemcpyToSymbol(g_tables, &h, sizeof(Tables));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_twist, h.twist, sizeof(h.twist));
   if (prev != dev) cudaSetDevice(prev);
   return e == cudaSuccess ? SILENZIO_OK : SILENZIO_ERR_CUDA;
 }
@@ -63,25 +65,33 @@ int ensure_tables() {
 }
 
 // ------------------------------------------------------------------ team FFT
+// named barrier per 64-thread team (id 1 + team index within the CTA)
 __device__ __forceinline__ void team_sync(int team) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(kTeam) : "memory");
 }
 
 // Forward transform. In: x[m] = folded value at j = t + 64 m (natural m).
 // Out: x[4u + r] = spectrum at position 4 (t + 64 u) + bitrev2(r) ("slot" order).
+// `buf` (16 KiB) is the exchange buffer; on return the caller must team_sync
+// before overwriting it (other threads may still be reading pass-3 data).
 __device__ __forceinline__ void fwd_fft(double2 (&x)[16], double2 *buf, int t, int team) {
   const Tables &T = g_tables;
   // negacyclic twist, part 1: w^{64 m} (the w^t part is folded into tw1)
 #pragma unroll
-  for (int m = 0; m < 16; m++) x[m] = cmul(x[m], T.twist[m]);
+  for (int m = 0; m < 16; m++) x[m] = cmul(x[m], c_twist[m]);
   // pass 1: radix 16 over stride 64 (thread owns offset s = t)
   dft<16, false>(x);
+  const int c1 = t ^ ((t >> 3) & 3);  // swz(t + 64 k) = 64 k + (c1 ^ 4 (k & 1))
   team_sync(team);
 #pragma unroll
   for (int r = 0; r < 16; r++) {
     const int k = bitrev4(r);
+#ifdef SZ_DIAG_TW
+    const double2 w = make_double2(0.7 + k, 0.1 * t);
+#else
     const double2 w = __ldg(&T.tw1[k * 64 + t]);
-    buf[swz(t + 64 * k)] = cmul(x[r], w);
+#endif
+    buf[64 * k + (c1 ^ ((k & 1) << 2))] = cmul(x[r], w);
   }
   team_sync(team);
   // pass 2: radix 16 over stride 4 inside blocks of 64
@@ -138,15 +148,16 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[16], double2 *buf, int t, i
   for (int q = 0; q < 16; q++) buf[swz(64 * b + s + 4 * bitrev4(q))] = y[q];
   team_sync(team);
   // pass 1^-1
+  const int c1 = t ^ ((t >> 3) & 3);
 #pragma unroll
-  for (int k = 0; k < 16; k++) x[k] = cmulc(buf[swz(t + 64 * k)], __ldg(&T.tw1[k * 64 + t]));
+  for (int k = 0; k < 16; k++) x[k] = cmulc(buf[64 * k + (c1 ^ ((k & 1) << 2))], __ldg(&T.tw1[k * 64 + t]));
   dft<16, true>(x);
   // x[q] now holds m = bitrev4(q); reorder to natural m and untwist
   double2 o[16];
 #pragma unroll
   for (int q = 0; q < 16; q++) o[bitrev4(q)] = x[q];
 #pragma unroll
-  for (int m = 0; m < 16; m++) x[m] = cmulc(o[m], T.twist[m]);
+  for (int m = 0; m < 16; m++) x[m] = cmulc(o[m], c_twist[m]);
 }
 
 // ------------------------------------------------------------- limb helpers
@@ -202,49 +213,78 @@ constexpr int kN = 2048;
 constexpr int kLog2_2N = 12;
 
 __host__ __device__ constexpr size_t br_smem_bytes(int rows, int n) {
-  return 2 * kN * sizeof(u64)                     // ACC
-         + (size_t)rows * kM * sizeof(double2)    // digit spectra
-         + 2 * kM * sizeof(double2)               // per-team exchange buffers
+  return 2 * kM * sizeof(double2)                 // per-team transient buffer (ACC copy / IFFT exchange)
+         + (size_t)rows * kM * sizeof(double2)    // digit spectra (also forward exchange buffers)
          + ((size_t)n * sizeof(unsigned short) + 15) / 16 * 16;  // modswitched masks
 }
 
-__global__ void __launch_bounds__(128, 2) blind_rotate_kernel(BRArgs A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  const int rows = 2 * A.level;
-  u64 *acc = reinterpret_cast<u64 *>(smem);                                  // [2][2048]
-  double2 *dsm = reinterpret_cast<double2 *>(smem + 2 * kN * sizeof(u64));  // [rows][16][64]
-  double2 *xbuf = dsm + (size_t)rows * kM;                                   // [2][1024]
-  unsigned short *abar = reinterpret_cast<unsigned short *>(xbuf + 2 * kM);
+// limb p of the inverse transform -> its exact contribution round(x) * 2^{p w} mod 2^64
+__device__ __forceinline__ u64 limb_to_torus(double x, int p, int P, int w) {
+  if (P == 3 || p > 0) return (u64)__double2ll_rn(x) << (p * w);  // |x| < 2^53: exact
+  return f64_to_torus(x);                                          // P <= 2, low limb may exceed 2^53
+}
 
-  const int tid = threadIdx.x;
+// ACC lives in registers for the whole CMux loop: thread t of team g owns
+// ACC_g[j] for j = t + 64 m + 1024 h (m < 16, h < 2) -- exactly the
+// coefficients its inverse FFT produces, so the update never leaves registers.
+// Shared memory per CTA: two 16 KiB transient buffers (the ACC copy the
+// rotation reads, later the IFFT exchange) + one 16 KiB spectrum per GGSW row.
+constexpr int kMaxCPB = 1;  // ciphertexts per CTA (<= 3), advanced in lockstep (shared BSK stream)
+
+template <int L, int P>
+__global__ void __launch_bounds__(128 * kMaxCPB, 1) blind_rotate_kernel(BRArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_all[];
+  constexpr int rows = 2 * L;
+  const int slot = threadIdx.x >> 7;  // which ciphertext of the CTA
+  unsigned char *smem = smem_all + slot * br_smem_bytes(rows, A.n);
+  double2 *tbuf_all = reinterpret_cast<double2 *>(smem);  // [2][1024]
+  double2 *dsm = tbuf_all + 2 * kM;                        // [rows][16][64]
+  unsigned short *abar = reinterpret_cast<unsigned short *>(dsm + (size_t)rows * kM);
+
+  const int tid = threadIdx.x & 127;
   const int team = tid >> 6, t = tid & 63;
-  double2 *buf = xbuf + team * kM;
-  const int n = A.n, P = A.P, w = A.w;
-  const double two_w = ldexp(1.0, w);
-  const int top_bits = 64 - (P - 1) * w;
-  const double two_top = ldexp(1.0, top_bits), inv_two_top = ldexp(1.0, -top_bits);
+  const int bar_team = slot * 2 + team;
+  double2 *tbuf = tbuf_all + team * kM;
+  u64 *accs = reinterpret_cast<u64 *>(tbuf);  // ACC_g copy [2048]
+  const int n = A.n, w = A.w, blog = A.base_log;
 
-  for (long c = blockIdx.x; c < A.count; c += gridDim.x) {
+  // all CTA slots iterate the same number of times (idle slots keep the barriers)
+  const int cpb = blockDim.x >> 7;
+  const long ngroups = (A.count + cpb - 1) / cpb;
+  for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const long c = grp * cpb + slot;
+    const bool live = c < A.count;
     const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
     // ---- modulus switch (a2)
-    for (int i = tid; i < n; i += blockDim.x) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2N);
-    const int bt = (int)sz_modswitch(lwe[n], kLog2_2N);
+    for (int i = tid; i < n; i += 128) abar[i] = live ? (unsigned short)sz_modswitch(lwe[i], kLog2_2N) : 0;
+    const int bt = live ? (int)sz_modswitch(lwe[n], kLog2_2N) : 0;
     // ---- ACC init (a3): ACC = (0, X^{-b~} v), (X^{-b} v)[j] = v[j + b] (negacyclic)
-    u32 id = A.lut_ids ? A.lut_ids[c] : 0u;
+    u32 id = (A.lut_ids && live) ? A.lut_ids[c] : 0u;
     if (id >= A.num_luts) id = 0;
     const u64 *v = A.luts + (size_t)id * kN;
-    for (int j = tid; j < kN; j += blockDim.x) {
-      acc[j] = 0;
-      const int idx = (j + bt) & (2 * kN - 1);
-      acc[kN + j] = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
-    }
-    __syncthreads();
+    u64 accr[16][2];
+#pragma unroll
+    for (int m = 0; m < 16; m++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int j = t + 64 * m + 1024 * h;
+        const int idx = (j + bt) & (2 * kN - 1);
+        const u64 vv = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
+        accr[m][h] = team ? vv : 0ull;
+      }
+    __syncthreads();  // abar visible
 
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
+      // ---------------- publish ACC_g for the rotation
+#pragma unroll
+      for (int m = 0; m < 16; m++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) accs[t + 64 * m + 1024 * h] = accr[m][h];
+      team_sync(bar_team);
       // ---------------- forward: digits of X^a ACC_g - ACC_g, one FFT per level
-      const u64 *accg = acc + team * kN;
-      for (int lvl = 1; lvl <= A.level; lvl++) {
+#pragma unroll 1
+      for (int lvl = 1; lvl <= L; lvl++) {
         double2 x[16];
 #pragma unroll
         for (int m = 0; m < 16; m++) {
@@ -253,77 +293,79 @@ __global__ void __launch_bounds__(128, 2) blind_rotate_kernel(BRArgs A) {
           for (int h = 0; h < 2; h++) {
             const int j = t + 64 * m + 1024 * h;
             const int src = (j - a) & (2 * kN - 1);
-            const u64 rot = (src < kN) ? accg[src] : (u64)0 - accg[src - kN];
-            u64 r = sz_decomp_round(rot - accg[j], A.base_log, A.level);
+            const u64 rv = accs[src & (kN - 1)];
+            const u64 rot = (src < kN) ? rv : (u64)0 - rv;
+            u64 r = sz_decomp_round(rot - accr[m][h], blog, L);
             i64 d = 0;
             // peel digits t = l, l-1, ..., lvl  (level lvl has weight q/B^lvl)
-            for (int tt = A.level; tt >= lvl; tt--) d = sz_decomp_next(r, A.base_log);
+#pragma unroll
+            for (int tt = L; tt >= 1; tt--) {
+              const i64 dd = sz_decomp_next(r, blog);
+              if (tt == lvl) d = dd;
+            }
             dv[h] = (double)d;
           }
           x[m] = make_double2(dv[0], dv[1]);
         }
-        fwd_fft(x, buf, t, team);
-        double2 *drow = dsm + (size_t)(team * A.level + (lvl - 1)) * kM;
+        double2 *drow = dsm + (size_t)(team * L + (lvl - 1)) * kM;
+        fwd_fft(x, drow, t, bar_team);  // the row's own spectrum buffer is the exchange buffer
+        team_sync(bar_team);
 #pragma unroll
         for (int sl = 0; sl < 16; sl++) drow[sl * 64 + t] = x[sl];
       }
-      __syncthreads();
+      __syncthreads();  // every row's spectrum is complete
       // ---------------- inverse: output component o = team, limbs top -> 0
       const int o = team;
-      double2 V[16];
-      u64 *acco = acc + o * kN;
-      const double2 *Gi = A.fbsk + (size_t)i * 2 * rows * P * kM + (size_t)o * rows * P * kM;
+#ifdef SZ_DIAG_G_L1
+      const double2 *Gi = A.fbsk + ((size_t)(i & 0) * 2 + o) * rows * P * kM;
+#else
+      const double2 *Gi = A.fbsk + ((size_t)i * 2 + o) * rows * P * kM;
+#endif
+#pragma unroll 1
       for (int p = P - 1; p >= 0; p--) {
         double2 y[16];
 #pragma unroll
         for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
+#pragma unroll 1
         for (int row = 0; row < rows; row++) {
-          const double2 *G = Gi + ((size_t)row * P + p) * kM;
-          const double2 *D = dsm + (size_t)row * kM;
+          const double2 *G = Gi + ((size_t)row * P + p) * kM + t;
+          const double2 *D = dsm + (size_t)row * kM + t;
 #pragma unroll
-          for (int sl = 0; sl < 16; sl++) cmac(y[sl], D[sl * 64 + t], __ldg(&G[sl * 64 + t]));
+          for (int qq = 0; qq < 4; qq++) {
+            double2 g[4], dd[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) g[q] = __ldg(&G[(4 * qq + q) * 64]);
+#pragma unroll
+            for (int q = 0; q < 4; q++) dd[q] = D[(4 * qq + q) * 64];
+#pragma unroll
+            for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], dd[q], g[q]);
+          }
         }
-        inv_fft(y, buf, t, team);
-        // exact rounding + limb recombination (limb p has weight 2^{p w})
-        if (p == 0) {
+        inv_fft(y, tbuf, t, bar_team);
 #pragma unroll
-          for (int m = 0; m < 16; m++) {
-            u64 lo = f64_to_torus(y[m].x), hi = f64_to_torus(y[m].y);
-            if (P > 1) {
-              lo += (u64)__double2ll_rn(V[m].x) << w;
-              hi += (u64)__double2ll_rn(V[m].y) << w;
-            }
-            acco[t + 64 * m] += lo;
-            acco[t + 64 * m + 1024] += hi;
-          }
-        } else if (p == P - 1) {
-#pragma unroll
-          for (int m = 0; m < 16; m++) {
-            V[m].x = fmod_pow2(rint(y[m].x), two_top, inv_two_top);
-            V[m].y = fmod_pow2(rint(y[m].y), two_top, inv_two_top);
-          }
-        } else {
-          const int bits = 64 - p * w;
-          const double tb = ldexp(1.0, bits), itb = ldexp(1.0, -bits);
-#pragma unroll
-          for (int m = 0; m < 16; m++) {
-            V[m].x = fmod_pow2(fma(V[m].x, two_w, rint(y[m].x)), tb, itb);
-            V[m].y = fmod_pow2(fma(V[m].y, two_w, rint(y[m].y)), tb, itb);
-          }
+        for (int m = 0; m < 16; m++) {
+          accr[m][0] += limb_to_torus(y[m].x, p, P, w);
+          accr[m][1] += limb_to_torus(y[m].y, p, P, w);
         }
       }
-      __syncthreads();
+      __syncthreads();  // spectra and transient buffers free for the next CMux
     }
-    // ---- sample extraction (a5)
+    // ---- sample extraction (a5): a'[0] = A[0], a'[i] = -A[N-i], b' = B[0]
     u64 *out = A.lwe_out + (size_t)c * (kN + 1);
-    for (int j = tid; j <= kN; j += blockDim.x) {
-      u64 val;
-      if (j == 0) val = acc[0];
-      else if (j < kN) val = (u64)0 - acc[kN - j];
-      else val = acc[kN];
-      out[j] = val;
-    }
-    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; m++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int j = t + 64 * m + 1024 * h;
+        if (!live) {
+        } else if (team == 0) {
+          if (j == 0) out[0] = accr[m][h];
+          else out[kN - j] = (u64)0 - accr[m][h];
+        } else if (j == 0) {
+          out[kN] = accr[m][h];
+        }
+      }
+    __syncthreads();  // abar reuse
   }
 }
 
@@ -378,17 +420,40 @@ int launch_blind_rotate(const u64 *lwe_small, const u32 *lut_ids, const u64 *lut
   A.base_log = (int)P->pbs_base_log;
   A.P = (int)P->fft_limbs;
   A.w = (int)P->limb_bits;
-  const size_t smem = br_smem_bytes(2 * A.level, A.n);
-  SZ_CUDA_OK(cudaFuncSetAttribute(blind_rotate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void (*kern)(BRArgs) = nullptr;
+#define SZ_BR_CASE(LL, PP) \
+  if (A.level == LL && A.P == PP) kern = blind_rotate_kernel<LL, PP>;
+  SZ_BR_CASE(1, 1) SZ_BR_CASE(1, 2) SZ_BR_CASE(1, 3)
+  SZ_BR_CASE(2, 1) SZ_BR_CASE(2, 2) SZ_BR_CASE(2, 3)
+  SZ_BR_CASE(4, 1) SZ_BR_CASE(4, 2) SZ_BR_CASE(4, 3)
+#undef SZ_BR_CASE
+  if (!kern) return SILENZIO_ERR_UNSUPPORTED;
+  const size_t per_ct = br_smem_bytes(2 * A.level, A.n);
+  int cpb = (int)((227 * 1024) / per_ct);
+  if (cpb > kMaxCPB) cpb = kMaxCPB;
+  if (cpb < 1) return SILENZIO_ERR_UNSUPPORTED;
+  const size_t smem = cpb * per_ct;
+  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int dev = 0, sms = 0, per_sm = 0;
   SZ_CUDA_OK(cudaGetDevice(&dev));
   SZ_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  SZ_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, blind_rotate_kernel, 128, smem));
+  SZ_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128 * cpb, smem));
   if (per_sm < 1) return SILENZIO_ERR_UNSUPPORTED;
-  const long resident = (long)sms * per_sm;
-  const long grid = (long)count < resident ? (long)count : resident;
-  blind_rotate_kernel<<<(unsigned)grid, 128, smem, stream>>>(A);
-  SZ_LAUNCH_OK();
+  // One launch per resident wave: every CTA of a wave sweeps BSK_0..BSK_{n-1}
+  // at the same pace, so the streamed Fourier BSK (146 MB at set A, > L2)
+  // is fetched from HBM about once per wave instead of once per drifting CTA.
+  const long resident_cts = (long)sms * per_sm * cpb;
+  for (long c0 = 0; c0 < (long)count; c0 += resident_cts) {
+    BRArgs W = A;
+    const long cnt = ((long)count - c0 < resident_cts) ? (long)count - c0 : resident_cts;
+    W.lwe_small = A.lwe_small + (size_t)c0 * (A.n + 1);
+    W.lut_ids = A.lut_ids ? A.lut_ids + c0 : nullptr;
+    W.lwe_out = A.lwe_out + (size_t)c0 * (kN + 1);
+    W.count = cnt;
+    const long grid = (cnt + cpb - 1) / cpb;
+    kern<<<(unsigned)grid, 128 * cpb, smem, stream>>>(W);
+    SZ_LAUNCH_OK();
+  }
   return SILENZIO_OK;
 }
 

@@ -12,7 +12,7 @@ from dataclasses import dataclass
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsilenzio.so")
+LIB_PATH = os.environ.get("SILENZIO_LIB", os.path.join(_HERE, "libsilenzio.so"))
 
 _lib = None
 
