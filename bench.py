@@ -286,6 +286,7 @@ def main():
         return
 
     flops = pbs_flops(P)
+    launches = int(args.steps * silenzio.pbs_launch_count(P, B))
     br_avg_s = float(np.mean(br_ms)) / 1e3
     achieved = flops * B / br_avg_s / 1e12
     roofline = {"bound": "alu", "pipe": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
@@ -304,7 +305,7 @@ def main():
                        "limb_bits": P.limb_bits, "parallelism": f"dp{world} (independent ciphertexts)",
                        "l2": f"inputs {B * (P.big_dim + 1) * 8 / 1e9:.2f} GB per step > 126 MB L2, no flush needed",
                        "decrypt_failures": failures},
-            "roofline": roofline, "gpu_launches": 2 * args.steps, "clocks": clk}
+            "roofline": roofline, "gpu_launches": launches, "clocks": clk}
     if e2e is not None:
         line["e2e"] = e2e
     if not args.no_cpu_baseline and world == 1:

@@ -72,6 +72,11 @@ size_t silenzio_fourier_bsk_bytes(const silenzio_params *params);
  * (the keyswitched small-key LWEs, count*(n+1)*8, rounded up). */
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *params, size_t count);
 
+/* Number of kernel launches silenzio_pbs_batch makes for `count` ciphertexts:
+ * one keyswitch plus one blind rotation per resident wave (all CTAs of a wave
+ * sweep the Fourier BSK together). -1 if the parameters are unsupported. */
+long silenzio_pbs_launch_count(const silenzio_params *params, size_t count);
+
 /* ------------------------------------------------------- hot-path calls */
 /* BSK -> Fourier (offline, once per key).
  *  bsk          [n][(k+1)l][k+1][N] u64, standard domain (GGSW of s_i, C6).

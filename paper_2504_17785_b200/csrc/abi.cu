@@ -9,6 +9,7 @@ namespace sz {
 int launch_blind_rotate(const u64 *, const u32 *, const u64 *, u32, const void *, u64 *, size_t,
                         const silenzio_params *, cudaStream_t);
 int launch_bsk_to_fourier(const u64 *, void *, const silenzio_params *, cudaStream_t);
+long blind_rotate_wave(const silenzio_params *);
 int launch_keyswitch(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, cudaStream_t);
 int launch_lwe_encrypt(const u64 *, const i64 *, const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_lwe_phase(const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
@@ -142,6 +143,14 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
                              (int)P->ks_level, sz_stream(stream))))
     return st;
   return silenzio_blind_rotate_batch(small, lut_ids, luts, num_luts, fbsk, out, count, P, stream);
+}
+
+long silenzio_pbs_launch_count(const silenzio_params *P, size_t count) {
+  if (check_params(P) != SILENZIO_OK || check_br_supported(P) != SILENZIO_OK) return -1;
+  if (count == 0) return 0;
+  const long wave = blind_rotate_wave(P);
+  if (wave <= 0) return -1;
+  return 1 + (long)((count + wave - 1) / wave);  // keyswitch + one blind rotation per wave
 }
 
 size_t silenzio_pbs_host_workspace_bytes(const silenzio_params *P, size_t chunk) {

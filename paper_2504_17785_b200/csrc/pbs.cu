@@ -229,10 +229,13 @@ __device__ __forceinline__ u64 limb_to_torus(double x, int p, int P, int w) {
 // coefficients its inverse FFT produces, so the update never leaves registers.
 // Shared memory per CTA: two 16 KiB transient buffers (the ACC copy the
 // rotation reads, later the IFFT exchange) + one 16 KiB spectrum per GGSW row.
-constexpr int kMaxCPB = 1;  // ciphertexts per CTA (<= 3), advanced in lockstep (shared BSK stream)
+constexpr int kMaxCPB = 1;  // ciphertexts per CTA (lockstep CTAs measured slower: shared stalls)
+#ifndef SZ_BR_MINBLOCKS
+#define SZ_BR_MINBLOCKS 2
+#endif
 
 template <int L, int P>
-__global__ void __launch_bounds__(128 * kMaxCPB, 1) blind_rotate_kernel(BRArgs A) {
+__global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_kernel(BRArgs A) {
   extern __shared__ __align__(16) unsigned char smem_all[];
   constexpr int rows = 2 * L;
   const int slot = threadIdx.x >> 7;  // which ciphertext of the CTA
@@ -402,6 +405,48 @@ __global__ void __launch_bounds__(64) bsk_to_fourier_kernel(B2FArgs A) {
 }
 
 // ------------------------------------------------------------ host launch
+// Kernel variant, CTA shape and resident ciphertexts per wave for these params.
+struct BRPlan {
+  void (*kern)(BRArgs);
+  int cpb;
+  size_t smem;
+  long wave;  // ciphertexts per launch (resident on the whole GPU)
+};
+
+static int plan_blind_rotate(const silenzio_params *P, BRPlan *plan) {
+  const int level = (int)P->pbs_level, limbs = (int)P->fft_limbs, n = (int)P->lwe_dim;
+  void (*kern)(BRArgs) = nullptr;
+#define SZ_BR_CASE(LL, PP) \
+  if (level == LL && limbs == PP) kern = blind_rotate_kernel<LL, PP>;
+  SZ_BR_CASE(1, 1) SZ_BR_CASE(1, 2) SZ_BR_CASE(1, 3)
+  SZ_BR_CASE(2, 1) SZ_BR_CASE(2, 2) SZ_BR_CASE(2, 3)
+  SZ_BR_CASE(4, 1) SZ_BR_CASE(4, 2) SZ_BR_CASE(4, 3)
+#undef SZ_BR_CASE
+  if (!kern) return SILENZIO_ERR_UNSUPPORTED;
+  const size_t per_ct = br_smem_bytes(2 * level, n);
+  int cpb = (int)((227 * 1024) / per_ct);
+  if (cpb > kMaxCPB) cpb = kMaxCPB;
+  if (cpb < 1) return SILENZIO_ERR_UNSUPPORTED;
+  const size_t smem = cpb * per_ct;
+  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 0, per_sm = 0;
+  SZ_CUDA_OK(cudaGetDevice(&dev));
+  SZ_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  SZ_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128 * cpb, smem));
+  if (per_sm < 1) return SILENZIO_ERR_UNSUPPORTED;
+  plan->kern = kern;
+  plan->cpb = cpb;
+  plan->smem = smem;
+  plan->wave = (long)sms * per_sm * cpb;
+  return SILENZIO_OK;
+}
+
+long blind_rotate_wave(const silenzio_params *P) {
+  BRPlan plan;
+  if (ensure_tables() != SILENZIO_OK || plan_blind_rotate(P, &plan) != SILENZIO_OK) return -1;
+  return plan.wave;
+}
+
 int launch_blind_rotate(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
                         const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
                         cudaStream_t stream) {
@@ -420,29 +465,15 @@ int launch_blind_rotate(const u64 *lwe_small, const u32 *lut_ids, const u64 *lut
   A.base_log = (int)P->pbs_base_log;
   A.P = (int)P->fft_limbs;
   A.w = (int)P->limb_bits;
-  void (*kern)(BRArgs) = nullptr;
-#define SZ_BR_CASE(LL, PP) \
-  if (A.level == LL && A.P == PP) kern = blind_rotate_kernel<LL, PP>;
-  SZ_BR_CASE(1, 1) SZ_BR_CASE(1, 2) SZ_BR_CASE(1, 3)
-  SZ_BR_CASE(2, 1) SZ_BR_CASE(2, 2) SZ_BR_CASE(2, 3)
-  SZ_BR_CASE(4, 1) SZ_BR_CASE(4, 2) SZ_BR_CASE(4, 3)
-#undef SZ_BR_CASE
-  if (!kern) return SILENZIO_ERR_UNSUPPORTED;
-  const size_t per_ct = br_smem_bytes(2 * A.level, A.n);
-  int cpb = (int)((227 * 1024) / per_ct);
-  if (cpb > kMaxCPB) cpb = kMaxCPB;
-  if (cpb < 1) return SILENZIO_ERR_UNSUPPORTED;
-  const size_t smem = cpb * per_ct;
-  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int dev = 0, sms = 0, per_sm = 0;
-  SZ_CUDA_OK(cudaGetDevice(&dev));
-  SZ_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  SZ_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128 * cpb, smem));
-  if (per_sm < 1) return SILENZIO_ERR_UNSUPPORTED;
+  BRPlan plan;
+  if ((st = plan_blind_rotate(P, &plan))) return st;
+  void (*kern)(BRArgs) = plan.kern;
+  const int cpb = plan.cpb;
+  const size_t smem = plan.smem;
   // One launch per resident wave: every CTA of a wave sweeps BSK_0..BSK_{n-1}
   // at the same pace, so the streamed Fourier BSK (146 MB at set A, > L2)
   // is fetched from HBM about once per wave instead of once per drifting CTA.
-  const long resident_cts = (long)sms * per_sm * cpb;
+  const long resident_cts = plan.wave;
   for (long c0 = 0; c0 < (long)count; c0 += resident_cts) {
     BRArgs W = A;
     const long cnt = ((long)count - c0 < resident_cts) ? (long)count - c0 : resident_cts;

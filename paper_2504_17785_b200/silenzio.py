@@ -43,6 +43,7 @@ def load():
         "silenzio_fourier_bsk_bytes": ([P], S),
         "silenzio_pbs_workspace_bytes": ([P, S], S),
         "silenzio_pbs_host_workspace_bytes": ([P, S], S),
+        "silenzio_pbs_launch_count": ([P, S], ctypes.c_long),
         "silenzio_bsk_to_fourier": ([V, V, P, V], I),
         "silenzio_keyswitch_batch": ([V, V, V, S, P, V], I),
         "silenzio_pbs_batch": ([V, V, V, U32, V, V, V, S, P, V, V], I),
@@ -66,7 +67,7 @@ def load():
 def exported_symbols():
     return [
         "silenzio_status_string", "silenzio_version", "silenzio_fourier_bsk_bytes",
-        "silenzio_pbs_workspace_bytes", "silenzio_pbs_host_workspace_bytes",
+        "silenzio_pbs_workspace_bytes", "silenzio_pbs_host_workspace_bytes", "silenzio_pbs_launch_count",
         "silenzio_bsk_to_fourier", "silenzio_keyswitch_batch", "silenzio_pbs_batch",
         "silenzio_blind_rotate_batch", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
         "silenzio_build_testpoly", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
@@ -131,6 +132,10 @@ def fourier_bsk_bytes(P) -> int:
 
 def pbs_workspace_bytes(P, count: int) -> int:
     return load().silenzio_pbs_workspace_bytes(ctypes.byref(make_params(P)), count)
+
+
+def pbs_launch_count(P, count: int) -> int:
+    return load().silenzio_pbs_launch_count(ctypes.byref(make_params(P)), count)
 
 
 def pbs_host_workspace_bytes(P, chunk: int) -> int:
