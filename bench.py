@@ -177,7 +177,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2504_17785_b200 import silenzio, workload as wl
+    from paper_2504_17785_b200 import dist as sdist, silenzio, workload as wl
     from synth import get_params, key_randomness, lut_ids, lut_tables, lwe_randomness, messages
 
     world, rank, local = dist_env()
@@ -195,7 +195,7 @@ def main():
     del rnd
     tabs = lut_tables(8, P.p, args.seed)
     luts = wl.luts_from_tables(tabs, P.p, P.N, dev)
-    in_seed = args.seed + 1000 * rank
+    in_seed = sdist.input_seed(args.seed, rank)
     ids_np = lut_ids(B, 8, in_seed)
     msgs = messages(B, P.p, in_seed)
     r = lwe_randomness(P, B, in_seed)
@@ -243,15 +243,10 @@ def main():
     total_ms = t_start.elapsed_time(t_end)
     ks_ms = [e[0].elapsed_time(e[1]) for e in evs]
     br_ms = [e[1].elapsed_time(e[2]) for e in evs]
-    if world > 1:
-        tt = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total_ms = float(tt.item())
-        fl = torch.tensor([failures], device=dev)
-        dist.all_reduce(fl)
-        failures = int(fl.item())
+    total_ms = sdist.max_over_ranks(total_ms, dev)
+    failures = sdist.sum_over_ranks(failures, dev)
     ms_per_step = total_ms / args.steps
-    value = world * B * args.steps / (total_ms / 1e3)
+    value = sdist.aggregate_throughput(world, B, args.steps, total_ms / 1e3)
 
     # ---- end-to-end through the public host-buffer entry point
     e2e = None
@@ -269,12 +264,9 @@ def main():
         for _ in range(args.steps):
             silenzio.pbs_batch_host(ct_h, ids_h, luts, keys["fbsk"], keys["ksk"], P, out_h, ws, chunk=chunk)
         e2e_s = time.perf_counter() - t0
-        if world > 1:
-            tt = torch.tensor([e2e_s], device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        e2e_s = sdist.max_over_ranks(e2e_s, dev)
         e2e_ok = bool(torch.equal(out_h, out.cpu()))
-        e2e = {"value": world * B * args.steps / e2e_s, "unit": UNIT,
+        e2e = {"value": sdist.aggregate_throughput(world, B, args.steps, e2e_s), "unit": UNIT,
                "h2d_bytes_per_step": int(B * (P.big_dim + 1) * 8 + B * 4),
                "d2h_bytes_per_step": int(B * (P.big_dim + 1) * 8),
                "api": "silenzio_pbs_batch_host (pinned host buffers, 16384-ciphertext chunks, copies overlapped)",

@@ -1,0 +1,43 @@
+"""Multi-GPU host logic: weak-scaling shards of independent ciphertexts.
+
+PBS ciphertexts are independent: each rank bootstraps its
+own batch with keys generated locally from the same key seed (replicated), so
+the data path has no collective. The only collectives are the barrier around
+the timed region and the max-over-ranks reduction of elapsed time.
+"""
+import torch
+import torch.distributed as dist
+
+
+def input_seed(seed: int, rank: int) -> int:
+    """Per-rank seed for ciphertext inputs (keys use `seed` on every rank)."""
+    return seed + 1000 * rank
+
+
+def shard_bounds(total: int, world: int, rank: int):
+    """Contiguous shard [lo, hi) of `total` independent ciphertexts for `rank`
+    (strong-scaling helper; bench.py uses weak scaling, one full batch per rank)."""
+    base, rem = divmod(total, world)
+    lo = rank * base + min(rank, rem)
+    return lo, lo + base + (1 if rank < rem else 0)
+
+
+def max_over_ranks(x: float, device=None) -> float:
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: int, device=None) -> int:
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return int(x)
+    t = torch.tensor([int(x)], dtype=torch.int64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())
+
+
+def aggregate_throughput(world: int, batch_per_rank: int, steps: int, max_seconds: float) -> float:
+    """Whole-job PBS/s: units all ranks processed / the slowest rank's time."""
+    return world * batch_per_rank * steps / max_seconds
