@@ -1,0 +1,135 @@
+"""Pins of the cleartext gadget reference (oracle/gadgets.py) against the
+paper's worked examples (tests/golden/, each with its citation), closed forms
+and brute force. No GPU."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import gadgets as G
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+BASE6 = [5, 7, 9, 11, 13, 16]  # BASELINE configs[3] base (R16)
+
+
+def gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def test_signed_encoding_paper_example():
+    # (0, 1, 2, -2, -1) -> (0, 1, 2, 3, 4) for M = 5
+    assert list(G.signed_encode([0, 1, 2, -2, -1], 5)) == [0, 1, 2, 3, 4]
+    assert list(G.signed_decode([0, 1, 2, 3, 4], 5)) == [0, 1, 2, -2, -1]
+    # R18: the element M/2 of an even ring is negative
+    assert int(G.signed_decode(8, 16)) == -8
+
+
+def test_rns2mrns_appendix_a():
+    g = gold("rns2mrns_appendix_a.json")
+    rns = G.to_rns(g["x"], g["moduli"])
+    assert list(rns) == g["rns"]
+    y, r = G.rns2mrns(rns, g["moduli"])
+    assert list(y) == g["mrns"] and r == g["moduli"]
+    assert int(G.mrns_value(y, r)) == g["x"]
+
+
+@pytest.mark.parametrize("moduli", [[5, 7, 8], [15, 14], [13, 15, 14], BASE6])
+def test_rns2mrns_exhaustive_roundtrip(moduli):
+    M = math.prod(moduli)
+    x = np.arange(M)
+    y, r = G.rns2mrns(G.to_rns(x, moduli), moduli)
+    assert all(((y[i] >= 0) & (y[i] < r[i])).all() for i in range(len(r)))
+    assert np.array_equal(G.mrns_value(y, r), x)
+
+
+def test_crt_matches_brute_force():
+    moduli = [5, 7, 9]
+    M = math.prod(moduli)
+    for x in range(M):
+        assert int(G.crt(G.to_rns(np.array([x]), moduli), moduli)[0]) == x
+
+
+def test_shift2msbs_paper_table():
+    g = gold("shift2msbs_table.json")
+    Xp = np.array(g["digits_least_significant_first"]).T  # axis 0 = digit index
+    Y, shift, dbg = G.shift2msbs_plus_mrns(Xp, g["w"], g["gamma"])
+    assert list(Y) == g["Y"] and shift == g["shift"]
+    assert dbg["maxBit"] == g["maxBit"]
+    assert list(dbg["digitShift"]) == g["digitShift"]
+    assert list(dbg["lshift"]) == g["lshift"] and list(dbg["rshift"]) == g["rshift"]
+
+
+def test_shift2msbs_small_values_pass_through():
+    # value 5 over radices (13, 15, 14) has digits (5, 0, 0): no shift,
+    # output 5, shift = 3 - 5 = -2 (needs the zero-digit reading R11)
+    base = [13, 15, 14]
+    for v in range(13):
+        Y, shift = G.shift2msbs_plus(G.to_rns(np.array([v]), base), base, 4, 5)
+        assert int(Y[0]) == v
+    Y, shift = G.shift2msbs_plus(G.to_rns(np.array([5]), base), base, 4, 5)
+    assert shift == -2
+
+
+@pytest.mark.parametrize("shape", [(2, 6, 2), (3, 31, 4), (4, 784, 3)])
+def test_matmul_rns_crt_equals_integer_matmul(shape):
+    a, b, c = shape
+    rng = np.random.default_rng(a * b * c)
+    X = rng.integers(-8, 8, size=(a, b))
+    W = rng.integers(-8, 8, size=(b, c))
+    Y = G.matmul_rns(X, W, BASE6)
+    M = math.prod(BASE6)
+    assert np.array_equal(G.signed_decode(G.crt(Y, BASE6), M), X @ W)
+
+
+def test_sign_rns_exhaustive_closed_form():
+    """Top MRNS digit >= r_k/2 <=> element >= M/2 (even r_k), over all of Z_M."""
+    M = math.prod(BASE6)
+    v = np.arange(M)
+    s = G.sign_rns(G.to_rns(v, BASE6), BASE6)
+    expect = np.where(2 * v >= M, -1, np.where(v == 0, 0, 1))
+    assert np.array_equal(s, expect)
+
+
+def test_shift2msbs_pm_output_range_and_sign():
+    rng = np.random.default_rng(1)
+    M = math.prod(BASE6)
+    for _ in range(50):
+        x = rng.integers(-50176, 50177, size=(4, 5))
+        Y, _ = G.shift2msbs_pm(G.to_rns(x, BASE6), BASE6, 4, 4)
+        assert np.abs(Y).max() <= 7
+        assert ((np.sign(Y) == np.sign(x)) | (Y == 0)).all()
+    assert M > 2 * 50176
+
+
+def test_exp_lut_endpoints():
+    # Fig. exp_approx / S:335-336: input 2^gamma - 1 -> 2^kappa, input 0 -> 0 (gamma=6, kappa=4)
+    assert int(G.exp_lut(63, 6, 4)) == 16 and int(G.exp_lut(0, 6, 4)) == 0
+
+
+def test_ce_gradient_uniform_logits_property():
+    # with uniform logits the label position gets a value in {-1, 0} and
+    # every other position a value in {0, 1}
+    Yhat = np.full((5, 10), 3)
+    Y = np.zeros((5, 10), dtype=np.int64)
+    Y[np.arange(5), [0, 3, 9, 2, 2]] = 1
+    E = G.int_ce_loss_deriv(Yhat, Y, gamma=6, kappa=4)
+    assert set(np.unique(E[Y == 1])) <= {-1, 0} and set(np.unique(E[Y == 0])) <= {0, 1}
+
+
+def test_ce_gradient_gamma3_kappa0_closed_form():
+    # R10/R12 at Gamma = 4 (gamma = 3), kappa = 0: E_i = 1 iff the clamped logit is 7
+    rng = np.random.default_rng(2)
+    Yhat = rng.integers(-8, 8, size=(64, 10))
+    Y = np.zeros((64, 10), dtype=np.int64)
+    Y[np.arange(64), rng.integers(0, 10, size=64)] = 1
+    E = G.int_ce_loss_deriv(Yhat, Y, gamma=3, kappa=0)
+    assert set(np.unique(E)) <= {-1, 0, 1}
+    assert not (E[Y == 1] == 1).any()
+    e1 = (np.maximum(Yhat, 0) == 7).astype(np.int64)
+    S = e1.sum(axis=1, keepdims=True)
+    Ehat = np.rint((e1 + 1) / (S + 1)).astype(np.int64)
+    Ehat = Ehat - Y * Ehat.sum(axis=1, keepdims=True)
+    assert np.array_equal(E, np.sign(Ehat))
