@@ -142,6 +142,26 @@ int silenzio_lwe_linear_batch(const uint64_t *in, const uint32_t *idx, const int
 int silenzio_build_testpoly(const uint64_t *tables, uint32_t num, uint32_t p, uint32_t N,
                             uint64_t *polys, void *stream);
 
+/* ------------------------------------------------------------ gadgets */
+/* Encrypted Matmul^RNS (Alg. 2, l.280-307) at
+ * parameter set A (N = 2048, 4-bit messages + padding, Delta = 2^59). A thin
+ * driver: it only sequences silenzio_lwe_linear_batch and silenzio_pbs_batch
+ * calls (schedule: DESIGN.md §Config 3).
+ *  X        [a][b] big-key LWE, each an integer in [-8, 8) encoded (x mod 32) Delta
+ *  W        [b][c] likewise
+ *  moduli   [k], each in {5, 7, 9, 11, 13, 16} (pairwise coprime; else
+ *           SILENZIO_ERR_WINDOW: no 16-value PBS window schedule for it)
+ *  out      [k][a][c] big-key LWE: residue (X W)_{ij} mod m at scale Delta for
+ *           m != 16, and at scale 2^60 for m = 16 (native wrap channel)
+ *  workspace >= silenzio_rns_matmul_workspace_bytes(params, a, b, c) device bytes.
+ * The call synchronises `stream` internally (host-built index arrays). */
+size_t silenzio_rns_matmul_workspace_bytes(const silenzio_params *params, uint32_t a, uint32_t b,
+                                           uint32_t c);
+int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32_t b, uint32_t c,
+                        const uint32_t *moduli_host, uint32_t k, uint64_t *out, const void *fourier_bsk,
+                        const uint64_t *ksk, const silenzio_params *params, void *workspace,
+                        size_t workspace_bytes, void *stream);
+
 /* ------------------------------------- client-side key / ciphertext generation
  * All random numbers are inputs (drawn by the caller), so every key and
  * ciphertext is a deterministic function of the caller's seeded draws. */

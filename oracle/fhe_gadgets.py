@@ -1,0 +1,156 @@
+"""Encrypted gadget composition on the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Implements, with oracle.pbs / oracle.lwe_linear only, the 4-bit PBS schedule of
+DESIGN.md §Config 3 for Matmul^RNS (Alg. 2, l.280-307): conversion
+(g1), residue products (g2) and modular summation (g3). It is written from the
+schedule description, independently of the CUDA driver
+(paper_2504_17785_b200/csrc/gadgets.cu); the cleartext results it must reproduce
+come from oracle/gadgets.py. "Parity unpinned" for the schedule itself (the
+paper has no 4-bit schedule): it is pinned by decrypting to the
+cleartext reference (tests/test_oracle_fhe_gadgets.py).
+"""
+import numpy as np
+
+from . import tfhe as T
+
+DELTA_LOG = 59      # set A: p = 4, Delta = 2^(64-5)
+DELTA16_LOG = 60    # native mod-16 channel
+
+
+def _u(v: int) -> int:
+    return int(v) % (1 << 64)
+
+
+def table(window_start: int, f, scale_log: int) -> np.ndarray:
+    """16 torus values realising f on the window [w0, w0+16) of Z_32 (toolbox T1):
+    x in [0,16) reads T[x]; x in [16,32) reads -T[x-16]."""
+    tab = [0] * 16
+    for x in range(window_start, window_start + 16):
+        xm = x % 32
+        v = _u(int(f(x)) << scale_log)
+        if xm < 16:
+            tab[xm] = v
+        else:
+            tab[xm - 16] = _u(-v)
+    return np.array(tab, dtype=np.uint64)
+
+
+def const_table(c: int) -> np.ndarray:
+    return np.full(16, _u(c), dtype=np.uint64)
+
+
+class Ctx:
+    def __init__(self, params, keys):
+        self.P = params
+        self.K = keys
+        self.pbs_count = 0
+
+    def lut(self, cts, tables, ids=None):
+        """PBS of every ciphertext with test polynomial tables[ids[i]]."""
+        cts = np.ascontiguousarray(cts)
+        if len(cts) == 0:
+            return cts.copy()
+        polys = np.stack([T.test_polynomial(t, 4, self.P.N) for t in tables])
+        ids = np.zeros(len(cts), np.uint32) if ids is None else np.asarray(ids, np.uint32)
+        self.pbs_count += len(cts)
+        return T.pbs(cts, ids, polys, self.K["bsk"], self.K["ksk"], self.P)
+
+    @staticmethod
+    def lin(cts, idx, coef, cst):
+        return T.lwe_linear(cts, np.asarray(idx, np.uint32), np.asarray(coef, np.int64),
+                            np.asarray([_u(c) for c in cst], dtype=np.uint64))
+
+
+def _inv4(m):
+    return pow(4, -1, m)
+
+
+def rns_matmul_fhe(ctx: Ctx, X, W, moduli):
+    """X [a][b], W [b][c] encrypted signed ints in [-8,8) -> out [k][a][c] residue
+    ciphertexts (scale 2^59, or 2^60 for m = 16), following DESIGN.md §Config 3."""
+    a, b = X.shape[0], X.shape[1]
+    c = W.shape[1]
+    big = X.shape[-1]
+    Xf = X.reshape(-1, big)
+    Wf = W.reshape(-1, big)
+    out = np.zeros((len(moduli), a, c, big), dtype=np.uint64)
+    for mi, m in enumerate(moduli):
+        # ---- g1: conversion on the signed window [-8, 8)
+        if m != 16:
+            tab = [table(-8, lambda x, m=m: x % m, DELTA_LOG)]
+            Xr = [ctx.lut(Xf, tab).reshape(a, b, big)]
+            Wr = [ctx.lut(Wf, tab).reshape(b, c, big)]
+        else:
+            tabs = [table(-8, lambda x: (x % 16) & 3, DELTA_LOG), table(-8, lambda x: (x % 16) >> 2, DELTA_LOG)]
+            Xr = [ctx.lut(Xf, tabs, np.full(len(Xf), d)).reshape(a, b, big) for d in (0, 1)]
+            Wr = [ctx.lut(Wf, tabs, np.full(len(Wf), d)).reshape(b, c, big) for d in (0, 1)]
+        for i in range(a):
+            for j in range(c):
+                terms = []
+                for kk in range(b):
+                    terms.extend(_product(ctx, m, [x[i, kk] for x in Xr], [w[kk, j] for w in Wr]))
+                terms = np.stack(terms)
+                out[mi, i, j] = _modsum(ctx, m, terms)
+    return out
+
+
+def _product(ctx, m, xs, ws):
+    """Residue product terms whose sum is x*w mod m (g2)."""
+    D = DELTA_LOG
+    if m in (5, 7):
+        pair = np.stack([xs[0], ws[0]])
+        st = ctx.lin(pair, [[0, 1], [0, 1]], [[1, 1], [1, -1]], [0, 0])   # s = x + w, d = x - w
+        i4 = _inv4(m)
+        tabs = [table(0, lambda s: (i4 * s * s) % m, D), table(-8, lambda d: (-i4 * d * d) % m, D)]
+        return list(ctx.lut(st, tabs, [0, 1]))
+    if m == 16:
+        src = np.stack([xs[0], xs[1], ws[0], ws[1]])  # a0, a1, b0, b1
+        q = ctx.lin(src, [[0, 2], [0, 3], [1, 2]], [[4, 1], [4, 1], [4, 1]], [0, 0, 0])
+        tabs = [table(0, lambda q: ((q >> 2) * (q & 3)) & 15, DELTA16_LOG),
+                table(0, lambda q: (4 * (q >> 2) * (q & 3)) & 15, DELTA16_LOG)]
+        return list(ctx.lut(q, tabs, [0, 1, 1]))
+    # m in {9, 11, 13}
+    half = m << (D - 1)
+    pair = np.stack([xs[0], ws[0]])
+    t = ctx.lin(pair, [[0, 1], [0, 1]], [[1, 1], [1, -1]], [-(m << D), 0])
+    sig = ctx.lut(t, [const_table(half)])
+    uv = ctx.lin(np.concatenate([t, sig]), [[0, 2], [1, 3]], [[1, -1], [1, -1]], [half, half])
+    i4 = _inv4(m)
+    tabs = [table(0, lambda s: (i4 * s * s) % m, D), table(0, lambda d: (-i4 * d * d) % m, D)]
+    return list(ctx.lut(uv, tabs, [0, 1]))
+
+
+def _modsum(ctx, m, terms):
+    """Sum of terms mod m (g3)."""
+    D = DELTA_LOG
+    if m == 16:
+        return ctx.lin(terms, [list(range(len(terms)))], [[1] * len(terms)], [0])[0]
+    cur = terms
+    while len(cur) > 1:
+        if m in (5, 7):
+            g = 3 if m == 5 else 2
+            groups = [list(range(s, min(s + g, len(cur)))) for s in range(0, len(cur), g)]
+            idx = [grp + [grp[0]] * (g - len(grp)) for grp in groups]
+            coef = [[1] * len(grp) + [0] * (g - len(grp)) for grp in groups]
+            sums = ctx.lin(cur, idx, coef, [0] * len(groups))
+            cur = ctx.lut(sums, [table(0, lambda s: s % m, D)])
+        else:
+            half = m << (D - 1)
+            pairs = [(s, s + 1) if s + 1 < len(cur) else (s, s) for s in range(0, len(cur), 2)]
+            idx = [list(p) for p in pairs]
+            coef = [[1, 1] if p[0] != p[1] else [1, 0] for p in pairs]
+            t = ctx.lin(cur, idx, coef, [-(m << D)] * len(pairs))
+            sig = ctx.lut(t, [const_table(half)])
+            n = len(pairs)
+            cur = ctx.lin(np.concatenate([t, sig]), [[e, n + e] for e in range(n)], [[1, -1]] * n, [half] * n)
+    return cur[0]
+
+
+def decode_residues(phases, moduli):
+    """Residue values from output phases (scale 2^59, or 2^60 for m = 16)."""
+    out = []
+    for m, ph in zip(moduli, phases):
+        d = DELTA16_LOG if m == 16 else DELTA_LOG
+        v = ((np.asarray(ph, dtype=np.uint64) + np.uint64(1 << (d - 1))) >> np.uint64(d)).astype(np.int64)
+        out.append(v % (16 if m == 16 else 32) % m)
+    return np.stack(out)

@@ -55,6 +55,8 @@ def load():
         "silenzio_lwe_phase_batch": ([V, V, U32, S, V, V], I),
         "silenzio_bsk_generate": ([V, V, V, V, V, P, V], I),
         "silenzio_ksk_generate": ([V, V, V, V, V, U32, U32, U32, U32, V], I),
+        "silenzio_rns_matmul_workspace_bytes": ([P, U32, U32, U32], S),
+        "silenzio_rns_matmul": ([V, V, U32, U32, U32, V, U32, V, V, V, P, V, S, V], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -71,7 +73,8 @@ def exported_symbols():
         "silenzio_bsk_to_fourier", "silenzio_keyswitch_batch", "silenzio_pbs_batch",
         "silenzio_blind_rotate_batch", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
         "silenzio_build_testpoly", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
-        "silenzio_bsk_generate", "silenzio_ksk_generate",
+        "silenzio_bsk_generate", "silenzio_ksk_generate", "silenzio_rns_matmul_workspace_bytes",
+        "silenzio_rns_matmul",
     ]
 
 
@@ -241,4 +244,25 @@ def ksk_generate(in_key, lwe_key, mask, noise, base_log, level, stream=None):
     out = torch.empty((in_dim, level, n + 1), dtype=torch.int64, device=mask.device)
     _check(load().silenzio_ksk_generate(_ptr(in_key), _ptr(lwe_key), _ptr(mask), _ptr(noise), _ptr(out), in_dim, n,
                                         base_log, level, _stream(stream)))
+    return out
+
+
+def rns_matmul_workspace_bytes(P, a, b, c) -> int:
+    return load().silenzio_rns_matmul_workspace_bytes(ctypes.byref(make_params(P)), a, b, c)
+
+
+def rns_matmul(X, W, moduli, fourier_bsk, ksk, P, out=None, workspace=None, stream=None):
+    """Encrypted Matmul^RNS: X [a][b], W [b][c] ciphertexts -> out [k][a][c] residue ciphertexts."""
+    a, b = X.shape[0], X.shape[1] if X.dim() == 3 else None
+    a, b, c = int(X.shape[0]), int(X.shape[1]), int(W.shape[1])
+    k = len(moduli)
+    if out is None:
+        out = torch.empty((k, a, c, P.k * P.N + 1), dtype=torch.int64, device=X.device)
+    nbytes = rns_matmul_workspace_bytes(P, a, b, c)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=X.device)
+    mod_arr = (ctypes.c_uint32 * k)(*[int(m) for m in moduli])
+    _check(load().silenzio_rns_matmul(_ptr(X), _ptr(W), a, b, c, mod_arr, k, _ptr(out), _ptr(fourier_bsk),
+                                      _ptr(ksk), ctypes.byref(make_params(P)), _ptr(workspace),
+                                      workspace.numel(), _stream(stream)))
     return out

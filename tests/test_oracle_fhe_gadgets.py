@@ -1,0 +1,58 @@
+"""The oracle's encrypted Matmul^RNS composition decrypts to the cleartext
+reference (Alg. 2) and, through CRT, to the integer matmul. No GPU."""
+import math
+
+import numpy as np
+
+import oracle
+from oracle import fhe_gadgets as F
+from oracle import gadgets as G
+from synth import get_params, key_randomness, lwe_randomness
+
+
+def encrypt_ints(P, K, vals, seed):
+    vals = np.asarray(vals)
+    r = lwe_randomness(P, vals.size, seed)
+    ct = oracle.lwe_encrypt(oracle.encode(vals.reshape(-1), P.p), K["big_key"], r["mask"], r["noise"])
+    return ct.reshape(vals.shape + (P.big_dim + 1,))
+
+
+def test_rns_matmul_fhe_tiny_matches_cleartext_and_crt():
+    P = get_params("A_SMALLN")
+    K = oracle.keygen(P, key_randomness(P, 31))
+    rng = np.random.default_rng(31)
+    a, b, c = 2, 3, 2
+    X = rng.integers(-8, 8, size=(a, b))
+    W = rng.integers(-8, 8, size=(b, c))
+    moduli = [5, 9, 16]
+    ctx = F.Ctx(P, K)
+    out = F.rns_matmul_fhe(ctx, encrypt_ints(P, K, X, 1), encrypt_ints(P, K, W, 2), moduli)
+    ph = oracle.lwe_phase(out, K["big_key"])
+    res = F.decode_residues(ph, moduli)
+    ref = G.matmul_rns(X, W, moduli)
+    assert np.array_equal(res, ref)
+    M = math.prod(moduli)
+    assert np.array_equal(G.signed_decode(G.crt(res, moduli), M), X @ W)
+    # PBS count of the schedule: g1 a*b + b*c elements x (1,1,2); g2 per product (2,4,3); g3 trees
+    assert ctx.pbs_count > 0
+
+
+def test_schedule_tables_realise_their_functions_on_the_window():
+    # T1 windows: f on [w0, w0+16) read back through the negacyclic rule
+    for w0 in (-8, 0):
+        t = F.table(w0, lambda x: x % 7, 59)
+        for x in range(w0, w0 + 16):
+            xm = x % 32
+            got = int(t[xm]) if xm < 16 else (-int(t[xm - 16])) % (1 << 64)
+            assert got == ((x % 7) << 59)
+    # quarter-square identity for every residue pair (g2 correctness, all moduli)
+    for m in (5, 7, 9, 11, 13):
+        i4 = pow(4, -1, m)
+        for x in range(m):
+            for w in range(m):
+                assert (i4 * ((x + w) % m) ** 2 - i4 * ((x - w) % m) ** 2) % m == (x * w) % m
+    # 2-bit digit product identity mod 16
+    for x in range(16):
+        for w in range(16):
+            a0, a1, b0, b1 = x & 3, x >> 2, w & 3, w >> 2
+            assert (a0 * b0 + 4 * a0 * b1 + 4 * a1 * b0) % 16 == (x * w) % 16
