@@ -10,6 +10,10 @@ int launch_blind_rotate(const u64 *, const u32 *, const u64 *, u32, const void *
                         const silenzio_params *, cudaStream_t);
 int launch_bsk_to_fourier(const u64 *, void *, const silenzio_params *, cudaStream_t);
 long blind_rotate_wave(const silenzio_params *);
+int launch_blind_rotate_large(const u64 *, const u32 *, const u64 *, u32, const void *, u64 *, size_t,
+                              const silenzio_params *, cudaStream_t);
+int launch_bsk_to_fourier_large(const u64 *, void *, const silenzio_params *, cudaStream_t);
+long blind_rotate_large_wave(const silenzio_params *);
 int launch_keyswitch(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, cudaStream_t);
 int launch_lwe_encrypt(const u64 *, const i64 *, const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_lwe_phase(const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
@@ -45,9 +49,16 @@ int check_params(const silenzio_params *P) {
 
 // Shapes the blind-rotation kernel implements (DESIGN.md §Kernels / §Scope).
 int check_br_supported(const silenzio_params *P) {
-  if (P->glwe_dim != 1 || P->poly_size != 2048) return SILENZIO_ERR_UNSUPPORTED;
-  if (P->pbs_level > 4 || P->lwe_dim > 4096) return SILENZIO_ERR_UNSUPPORTED;
-  return SILENZIO_OK;
+  if (P->glwe_dim != 1) return SILENZIO_ERR_UNSUPPORTED;
+  if (P->poly_size == 2048) {
+    if (P->pbs_level > 4 || P->pbs_level == 3 || P->lwe_dim > 4096) return SILENZIO_ERR_UNSUPPORTED;
+    return SILENZIO_OK;
+  }
+  if (P->poly_size == 8192) {
+    if (P->pbs_level > 4 || P->lwe_dim > 4096) return SILENZIO_ERR_UNSUPPORTED;
+    return SILENZIO_OK;
+  }
+  return SILENZIO_ERR_UNSUPPORTED;
 }
 
 int check_ks_params(const silenzio_params *P) {
@@ -57,7 +68,7 @@ int check_ks_params(const silenzio_params *P) {
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-const char *kVersion = "libsilenzio 0.1 (sm_100a, N=2048 blind rotation, P-limb exact FFT)";
+const char *kVersion = "libsilenzio 0.2 (sm_100a; blind rotation N=2048 and N=8192; P-limb exact FFT)";
 
 }  // namespace
 
@@ -97,6 +108,7 @@ int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fbsk, const silenzio_para
   if (!bsk || !fbsk) return SILENZIO_ERR_NULL_POINTER;
   if (!sz_aligned16(bsk) || !sz_aligned16(fbsk)) return SILENZIO_ERR_MISALIGNED;
   if ((st = check_br_supported(P))) return st;
+  if (P->poly_size == 8192) return launch_bsk_to_fourier_large(bsk, fbsk, P, sz_stream(stream));
   return launch_bsk_to_fourier(bsk, fbsk, P, sz_stream(stream));
 }
 
@@ -123,6 +135,8 @@ int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_i
   if (num_luts == 0) return SILENZIO_ERR_INVALID_PARAM;
   if (!sz_aligned16(fbsk)) return SILENZIO_ERR_MISALIGNED;
   if (count > (1ull << 31)) return SILENZIO_ERR_COUNT;
+  if (P->poly_size == 8192)
+    return launch_blind_rotate_large(lwe_small, lut_ids, luts, num_luts, fbsk, out, count, P, sz_stream(stream));
   return launch_blind_rotate(lwe_small, lut_ids, luts, num_luts, fbsk, out, count, P, sz_stream(stream));
 }
 
@@ -148,7 +162,7 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
 long silenzio_pbs_launch_count(const silenzio_params *P, size_t count) {
   if (check_params(P) != SILENZIO_OK || check_br_supported(P) != SILENZIO_OK) return -1;
   if (count == 0) return 0;
-  const long wave = blind_rotate_wave(P);
+  const long wave = P->poly_size == 8192 ? blind_rotate_large_wave(P) : blind_rotate_wave(P);
   if (wave <= 0) return -1;
   return 1 + (long)((count + wave - 1) / wave);  // keyswitch + one blind rotation per wave
 }

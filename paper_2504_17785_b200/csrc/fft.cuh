@@ -27,12 +27,6 @@ constexpr int kTeam = 64;     // threads per transform
 constexpr int kPts = 16;      // complex values per thread
 
 // e^{+2 pi i j / 16}, j = 0..15 (literal values, correctly rounded doubles)
-__device__ __constant__ double kCos16[16] = {
-    1.0, 0.92387953251128673848, 0.70710678118654757274, 0.38268343236508978178,
-    0.0, -0.38268343236508978178, -0.70710678118654757274, -0.92387953251128673848,
-    -1.0, -0.92387953251128673848, -0.70710678118654757274, -0.38268343236508978178,
-    0.0, 0.38268343236508978178, 0.70710678118654757274, 0.92387953251128673848};
-
 struct C16 {
   static constexpr double c[16] = {
       1.0, 0.92387953251128673848, 0.70710678118654757274, 0.38268343236508978178,

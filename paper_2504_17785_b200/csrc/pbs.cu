@@ -160,6 +160,79 @@ __device__ __forceinline__ void inv_fft(double2 (&x)[16], double2 *buf, int t, i
   for (int m = 0; m < 16; m++) x[m] = cmulc(o[m], c_twist[m]);
 }
 
+// Two inverse transforms interleaved (independent data, shared twiddle loads
+// and barriers): xa through buffer ba, xb through buffer bb.
+__device__ __forceinline__ void inv_fft2(double2 (&xa)[16], double2 (&xb)[16], double2 *ba, double2 *bb, int t,
+                                         int team) {
+  const Tables &T = g_tables;
+  team_sync(team);
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    double2 za[4], zb[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+      za[k] = xa[4 * u + bitrev2(k)];
+      zb[k] = xb[4 * u + bitrev2(k)];
+    }
+    dft<4, true>(za);
+    dft<4, true>(zb);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int pos = swz(4 * (t + 64 * u) + bitrev2(q));
+      ba[pos] = za[q];
+      bb[pos] = zb[q];
+    }
+  }
+  team_sync(team);
+  {
+    const int b = t >> 2, s = t & 3;
+    double2 ya[16], yb[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const int pos = swz(64 * b + s + 4 * k);
+      const double2 va = ba[pos], vb = bb[pos];
+      if (k == 0) {
+        ya[k] = va;
+        yb[k] = vb;
+      } else {
+        const double2 w = __ldg(&T.tw2[k * 4 + s]);
+        ya[k] = cmulc(va, w);
+        yb[k] = cmulc(vb, w);
+      }
+    }
+    dft<16, true>(ya);
+    dft<16, true>(yb);
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const int pos = swz(64 * b + s + 4 * bitrev4(q));
+      ba[pos] = ya[q];
+      bb[pos] = yb[q];
+    }
+  }
+  team_sync(team);
+  const int c1 = t ^ ((t >> 3) & 3);
+#pragma unroll
+  for (int k = 0; k < 16; k++) {
+    const int pos = 64 * k + (c1 ^ ((k & 1) << 2));
+    const double2 w = __ldg(&T.tw1[k * 64 + t]);
+    xa[k] = cmulc(ba[pos], w);
+    xb[k] = cmulc(bb[pos], w);
+  }
+  dft<16, true>(xa);
+  dft<16, true>(xb);
+  double2 oa[16], ob[16];
+#pragma unroll
+  for (int q = 0; q < 16; q++) {
+    oa[bitrev4(q)] = xa[q];
+    ob[bitrev4(q)] = xb[q];
+  }
+#pragma unroll
+  for (int m = 0; m < 16; m++) {
+    xa[m] = cmulc(oa[m], c_twist[m]);
+    xb[m] = cmulc(ob[m], c_twist[m]);
+  }
+}
+
 // ------------------------------------------------------------- limb helpers
 __device__ __forceinline__ i64 sext(i64 x, int bits) {
   return (bits >= 64) ? x : (i64)((u64)x << (64 - bits)) >> (64 - bits);
@@ -213,7 +286,7 @@ constexpr int kN = 2048;
 constexpr int kLog2_2N = 12;
 
 __host__ __device__ constexpr size_t br_smem_bytes(int rows, int n) {
-  return 2 * kM * sizeof(double2)                 // per-team transient buffer (ACC copy / IFFT exchange)
+  return 4 * kM * sizeof(double2)                 // two transient buffers per team (ACC copy / IFFT exchanges)
          + (size_t)rows * kM * sizeof(double2)    // digit spectra (also forward exchange buffers)
          + ((size_t)n * sizeof(unsigned short) + 15) / 16 * 16;  // modswitched masks
 }
@@ -240,14 +313,15 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
   constexpr int rows = 2 * L;
   const int slot = threadIdx.x >> 7;  // which ciphertext of the CTA
   unsigned char *smem = smem_all + slot * br_smem_bytes(rows, A.n);
-  double2 *tbuf_all = reinterpret_cast<double2 *>(smem);  // [2][1024]
-  double2 *dsm = tbuf_all + 2 * kM;                        // [rows][16][64]
+  double2 *tbuf_all = reinterpret_cast<double2 *>(smem);  // [2 teams][2][1024]
+  double2 *dsm = tbuf_all + 4 * kM;                        // [rows][16][64]
   unsigned short *abar = reinterpret_cast<unsigned short *>(dsm + (size_t)rows * kM);
 
   const int tid = threadIdx.x & 127;
   const int team = tid >> 6, t = tid & 63;
   const int bar_team = slot * 2 + team;
-  double2 *tbuf = tbuf_all + team * kM;
+  double2 *tbuf = tbuf_all + team * 2 * kM;
+  double2 *tbuf2 = tbuf + kM;
   u64 *accs = reinterpret_cast<u64 *>(tbuf);  // ACC_g copy [2048]
   const int n = A.n, w = A.w, blog = A.base_log;
 
@@ -325,30 +399,69 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
       const double2 *Gi = A.fbsk + ((size_t)i * 2 + o) * rows * P * kM;
 #endif
 #pragma unroll 1
-      for (int p = P - 1; p >= 0; p--) {
-        double2 y[16];
+      for (int p = P - 1; p >= 0; p -= 2) {
+        if (p >= 1) {
+          // limbs p and p-1 together: one pass over the spectra, two interleaved IFFTs
+          const int pa = p, pb = p - 1;
+          double2 ya[16], yb[16];
 #pragma unroll
-        for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
-#pragma unroll 1
-        for (int row = 0; row < rows; row++) {
-          const double2 *G = Gi + ((size_t)row * P + p) * kM + t;
-          const double2 *D = dsm + (size_t)row * kM + t;
-#pragma unroll
-          for (int qq = 0; qq < 4; qq++) {
-            double2 g[4], dd[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) g[q] = __ldg(&G[(4 * qq + q) * 64]);
-#pragma unroll
-            for (int q = 0; q < 4; q++) dd[q] = D[(4 * qq + q) * 64];
-#pragma unroll
-            for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], dd[q], g[q]);
+          for (int sl = 0; sl < 16; sl++) {
+            ya[sl] = make_double2(0.0, 0.0);
+            yb[sl] = make_double2(0.0, 0.0);
           }
-        }
-        inv_fft(y, tbuf, t, bar_team);
+#pragma unroll 1
+          for (int row = 0; row < rows; row++) {
+            const double2 *Ga = Gi + ((size_t)row * P + pa) * kM + t;
+            const double2 *Gb = Gi + ((size_t)row * P + pb) * kM + t;
+            const double2 *D = dsm + (size_t)row * kM + t;
 #pragma unroll
-        for (int m = 0; m < 16; m++) {
-          accr[m][0] += limb_to_torus(y[m].x, p, P, w);
-          accr[m][1] += limb_to_torus(y[m].y, p, P, w);
+            for (int qq = 0; qq < 4; qq++) {
+              double2 ga[4], gb[4], dd[4];
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                ga[q] = __ldg(&Ga[(4 * qq + q) * 64]);
+                gb[q] = __ldg(&Gb[(4 * qq + q) * 64]);
+              }
+#pragma unroll
+              for (int q = 0; q < 4; q++) dd[q] = D[(4 * qq + q) * 64];
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                cmac(ya[4 * qq + q], dd[q], ga[q]);
+                cmac(yb[4 * qq + q], dd[q], gb[q]);
+              }
+            }
+          }
+          inv_fft2(ya, yb, tbuf, tbuf2, t, bar_team);
+#pragma unroll
+          for (int m = 0; m < 16; m++) {
+            accr[m][0] += limb_to_torus(ya[m].x, pa, P, w) + limb_to_torus(yb[m].x, pb, P, w);
+            accr[m][1] += limb_to_torus(ya[m].y, pa, P, w) + limb_to_torus(yb[m].y, pb, P, w);
+          }
+        } else {
+          double2 y[16];
+#pragma unroll
+          for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
+#pragma unroll 1
+          for (int row = 0; row < rows; row++) {
+            const double2 *G = Gi + ((size_t)row * P + p) * kM + t;
+            const double2 *D = dsm + (size_t)row * kM + t;
+#pragma unroll
+            for (int qq = 0; qq < 4; qq++) {
+              double2 g[4], dd[4];
+#pragma unroll
+              for (int q = 0; q < 4; q++) g[q] = __ldg(&G[(4 * qq + q) * 64]);
+#pragma unroll
+              for (int q = 0; q < 4; q++) dd[q] = D[(4 * qq + q) * 64];
+#pragma unroll
+              for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], dd[q], g[q]);
+            }
+          }
+          inv_fft(y, tbuf, t, bar_team);
+#pragma unroll
+          for (int m = 0; m < 16; m++) {
+            accr[m][0] += limb_to_torus(y[m].x, p, P, w);
+            accr[m][1] += limb_to_torus(y[m].y, p, P, w);
+          }
         }
       }
       __syncthreads();  // spectra and transient buffers free for the next CMux

@@ -77,6 +77,14 @@ PARAMS = {
     "EXACT": Params("EXACT", n=16, k=1, N=512, pbs_base_log=16, pbs_level=4,
                     ks_base_log=8, ks_level=8, lwe_sigma_log2=NOISELESS,
                     glwe_sigma_log2=NOISELESS, p=2),
+    # Set-C-shaped (N=8192, 2^15 x 2, KS 2^4 x 4, 6-bit) with a small n for oracle replays.
+    "C_SMALLN": Params("C_SMALLN", n=12, k=1, N=8192, pbs_base_log=15, pbs_level=2,
+                       ks_base_log=4, ks_level=4, lwe_sigma_log2=-22.0,
+                       glwe_sigma_log2=-51.0, p=6),
+    "EXACT8192": Params("EXACT8192", n=4, k=1, N=8192, pbs_base_log=16,
+                        pbs_level=4, ks_base_log=8, ks_level=8,
+                        lwe_sigma_log2=NOISELESS, glwe_sigma_log2=NOISELESS,
+                        p=6),
     "EXACT2048": Params("EXACT2048", n=8, k=1, N=2048, pbs_base_log=16,
                         pbs_level=4, ks_base_log=8, ks_level=8,
                         lwe_sigma_log2=NOISELESS, glwe_sigma_log2=NOISELESS,
