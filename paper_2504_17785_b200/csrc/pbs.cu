@@ -22,6 +22,10 @@
 
 #include "fft.cuh"
 
+#ifndef SZ_PAIR_LIMBS
+#define SZ_PAIR_LIMBS 0  // limb pairs in the inverse: measured slower (17.3k vs 27.5k PBS/s, register pressure)
+#endif
+
 namespace sz {
 
 __device__ Tables g_tables;
@@ -286,7 +290,7 @@ constexpr int kN = 2048;
 constexpr int kLog2_2N = 12;
 
 __host__ __device__ constexpr size_t br_smem_bytes(int rows, int n) {
-  return 4 * kM * sizeof(double2)                 // two transient buffers per team (ACC copy / IFFT exchanges)
+  return (SZ_PAIR_LIMBS ? 4 : 2) * kM * sizeof(double2)  // transient buffers per team (ACC copy / IFFT exchanges)
          + (size_t)rows * kM * sizeof(double2)    // digit spectra (also forward exchange buffers)
          + ((size_t)n * sizeof(unsigned short) + 15) / 16 * 16;  // modswitched masks
 }
@@ -314,14 +318,14 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
   const int slot = threadIdx.x >> 7;  // which ciphertext of the CTA
   unsigned char *smem = smem_all + slot * br_smem_bytes(rows, A.n);
   double2 *tbuf_all = reinterpret_cast<double2 *>(smem);  // [2 teams][2][1024]
-  double2 *dsm = tbuf_all + 4 * kM;                        // [rows][16][64]
+  double2 *dsm = tbuf_all + (SZ_PAIR_LIMBS ? 4 : 2) * kM;  // [rows][16][64]
   unsigned short *abar = reinterpret_cast<unsigned short *>(dsm + (size_t)rows * kM);
 
   const int tid = threadIdx.x & 127;
   const int team = tid >> 6, t = tid & 63;
   const int bar_team = slot * 2 + team;
-  double2 *tbuf = tbuf_all + team * 2 * kM;
-  double2 *tbuf2 = tbuf + kM;
+  double2 *tbuf = tbuf_all + team * (SZ_PAIR_LIMBS ? 2 : 1) * kM;
+  double2 *tbuf2 = tbuf + kM;  // used only with SZ_PAIR_LIMBS
   u64 *accs = reinterpret_cast<u64 *>(tbuf);  // ACC_g copy [2048]
   const int n = A.n, w = A.w, blog = A.base_log;
 
@@ -399,8 +403,8 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
       const double2 *Gi = A.fbsk + ((size_t)i * 2 + o) * rows * P * kM;
 #endif
 #pragma unroll 1
-      for (int p = P - 1; p >= 0; p -= 2) {
-        if (p >= 1) {
+      for (int p = P - 1; p >= 0; p -= (SZ_PAIR_LIMBS ? 2 : 1)) {
+        if (SZ_PAIR_LIMBS && p >= 1) {
           // limbs p and p-1 together: one pass over the spectra, two interleaved IFFTs
           const int pa = p, pb = p - 1;
           double2 ya[16], yb[16];
