@@ -21,6 +21,7 @@
 #include <mutex>
 
 #include "fft.cuh"
+#include "tmem.cuh"
 
 #ifndef SZ_PAIR_LIMBS
 #define SZ_PAIR_LIMBS 0  // limb pairs in the inverse: measured slower (17.3k vs 27.5k PBS/s, register pressure)
@@ -72,6 +73,10 @@ int ensure_tables() {
 // named barrier per 64-thread team (id 1 + team index within the CTA)
 __device__ __forceinline__ void team_sync(int team) {
   asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(kTeam) : "memory");
+}
+// named barrier `id` over `count` threads (whole warps)
+__device__ __forceinline__ void bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // Forward transform. In: x[m] = folded value at j = t + 64 m (natural m).
@@ -274,6 +279,129 @@ __device__ __forceinline__ double fmod_pow2(double x, double two_bits, double in
   return fma(-floor(x * inv_two_bits), two_bits, x);
 }
 
+// ---------------------------------------------------------------- v3 (TMEM)
+// CTA = two ciphertexts x two 64-thread teams (256 threads). Warp w:
+// team g = w >> 2 (GLWE component), ciphertext slot cs = (w >> 1) & 1, half h = w & 1.
+// The two teams of a ciphertext sit on warps {2cs+h} and {4+2cs+h}, i.e. in the
+// same TMEM lane quadrant, so thread t of team 0 and thread t of team 1 own the
+// same TMEM lane. The digit spectra D^_0, D^_1 (one per team) are exchanged
+// through TMEM columns [0,64) and [64,128) instead of shared memory, and the
+// pass-1 twiddles w^{t(4k+1)} live in TMEM columns [128,192), so neither uses
+// the L1/shared-memory data path. Shared memory holds only the per-team
+// transient buffer (ACC copy for the rotation, then every FFT exchange).
+#ifndef SZ_TW_TMEM
+#define SZ_TW_TMEM 0  // twiddles from TMEM: measured slower in v2 (17.2k vs 27.6k PBS/s): tcgen05.ld latency
+#endif
+#ifndef SZ_V3
+#define SZ_V3 0  // TMEM spectrum exchange: measured slower (21.7k vs 27.6k PBS/s, TMEM load latency)
+#endif
+constexpr uint32_t kTmCols = 256, kColD = 0, kColTw = 128;
+
+__device__ __forceinline__ void fwd_fft_tm(double2 (&x)[16], double2 *buf, int t, int team, uint32_t tw_ta) {
+  const Tables &T = g_tables;
+#pragma unroll
+  for (int m = 0; m < 16; m++) x[m] = cmul(x[m], c_twist[m]);
+  dft<16, false>(x);
+  const int c1 = t ^ ((t >> 3) & 3);
+  team_sync(team);
+#if SZ_TW_TMEM
+#pragma unroll
+  for (int j = 0; j < 4; j += 2) {
+    uint32_t ra[16], rb[16];
+    tmem_ld16(tw_ta + 16 * j, ra);
+    tmem_ld16(tw_ta + 16 * (j + 1), rb);
+    tmem_wait_ld16x2(ra, rb);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int r = 4 * j + q, k = bitrev4(r);
+      buf[64 * k + (c1 ^ ((k & 1) << 2))] = cmul(x[r], unpack1(ra, q));
+      const int r2 = 4 * (j + 1) + q, k2 = bitrev4(r2);
+      buf[64 * k2 + (c1 ^ ((k2 & 1) << 2))] = cmul(x[r2], unpack1(rb, q));
+    }
+  }
+#else
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int k = bitrev4(r);
+    buf[64 * k + (c1 ^ ((k & 1) << 2))] = cmul(x[r], __ldg(&T.tw1[k * 64 + t]));
+  }
+#endif
+  team_sync(team);
+  const int b = t >> 2, s = t & 3;
+  double2 y[16];
+#pragma unroll
+  for (int m = 0; m < 16; m++) y[m] = buf[swz(64 * b + s + 4 * m)];
+  dft<16, false>(y);
+#pragma unroll
+  for (int r = 0; r < 16; r++) {
+    const int k = bitrev4(r);
+    buf[swz(64 * b + s + 4 * k)] = (k == 0) ? y[r] : cmul(y[r], __ldg(&T.tw2[k * 4 + s]));
+  }
+  team_sync(team);
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    double2 z[4];
+#pragma unroll
+    for (int m = 0; m < 4; m++) z[m] = buf[swz(4 * (t + 64 * u) + m)];
+    dft<4, false>(z);
+#pragma unroll
+    for (int r = 0; r < 4; r++) x[4 * u + r] = z[r];
+  }
+}
+
+__device__ __forceinline__ void inv_fft_tm(double2 (&x)[16], double2 *buf, int t, int team, uint32_t tw_ta) {
+  const Tables &T = g_tables;
+  team_sync(team);
+#pragma unroll
+  for (int u = 0; u < 4; u++) {
+    double2 z[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) z[k] = x[4 * u + bitrev2(k)];
+    dft<4, true>(z);
+#pragma unroll
+    for (int q = 0; q < 4; q++) buf[swz(4 * (t + 64 * u) + bitrev2(q))] = z[q];
+  }
+  team_sync(team);
+  {
+    const int b = t >> 2, s = t & 3;
+    double2 y[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+      const double2 v = buf[swz(64 * b + s + 4 * k)];
+      y[k] = (k == 0) ? v : cmulc(v, __ldg(&T.tw2[k * 4 + s]));
+    }
+    dft<16, true>(y);
+#pragma unroll
+    for (int q = 0; q < 16; q++) buf[swz(64 * b + s + 4 * bitrev4(q))] = y[q];
+  }
+  team_sync(team);
+  const int c1 = t ^ ((t >> 3) & 3);
+#if SZ_TW_TMEM
+#pragma unroll
+  for (int j = 0; j < 4; j += 2) {
+    uint32_t ra[16], rb[16];
+    tmem_ld16(tw_ta + 16 * j, ra);
+    tmem_ld16(tw_ta + 16 * (j + 1), rb);
+    tmem_wait_ld16x2(ra, rb);
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int k = bitrev4(4 * j + q), k2 = bitrev4(4 * (j + 1) + q);
+      x[k] = cmulc(buf[64 * k + (c1 ^ ((k & 1) << 2))], unpack1(ra, q));
+      x[k2] = cmulc(buf[64 * k2 + (c1 ^ ((k2 & 1) << 2))], unpack1(rb, q));
+    }
+  }
+#else
+#pragma unroll
+  for (int k = 0; k < 16; k++) x[k] = cmulc(buf[64 * k + (c1 ^ ((k & 1) << 2))], __ldg(&T.tw1[k * 64 + t]));
+#endif
+  dft<16, true>(x);
+  double2 o[16];
+#pragma unroll
+  for (int q = 0; q < 16; q++) o[bitrev4(q)] = x[q];
+#pragma unroll
+  for (int m = 0; m < 16; m++) x[m] = cmulc(o[m], c_twist[m]);
+}
+
 // ------------------------------------------------------------ BR kernel
 struct BRArgs {
   const u64 *lwe_small;  // [count][n+1]
@@ -328,6 +456,35 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
   double2 *tbuf2 = tbuf + kM;  // used only with SZ_PAIR_LIMBS
   u64 *accs = reinterpret_cast<u64 *>(tbuf);  // ACC_g copy [2048]
   const int n = A.n, w = A.w, blog = A.base_log;
+#if SZ_TW_TMEM
+  // pass-1 twiddles w^{t(4k+1)} of this thread's t in its own TMEM lane
+  // (64 columns per CTA): they leave the L1 data path entirely.
+  __shared__ uint32_t tmem_slot;
+  const int wid = threadIdx.x >> 5;
+  if (wid == 0) tmem_alloc(&tmem_slot, 64);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t ta_tw = tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16);
+#pragma unroll
+  for (int j = 0; j < 4; j++) {
+    double2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; q++) v[q] = g_tables.tw1[bitrev4(4 * j + q) * 64 + t];
+    uint32_t r16[16];
+    pack4(v, r16);
+    tmem_st16(ta_tw + 16 * j, r16);
+  }
+  tmem_wait_st();
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+#define SZ_FWD(x, b, tt, tm) fwd_fft_tm(x, b, tt, tm, ta_tw)
+#define SZ_INV(x, b, tt, tm) inv_fft_tm(x, b, tt, tm, ta_tw)
+#else
+#define SZ_FWD(x, b, tt, tm) fwd_fft(x, b, tt, tm)
+#define SZ_INV(x, b, tt, tm) inv_fft(x, b, tt, tm)
+#endif
 
   // all CTA slots iterate the same number of times (idle slots keep the barriers)
   const int cpb = blockDim.x >> 7;
@@ -389,7 +546,7 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
           x[m] = make_double2(dv[0], dv[1]);
         }
         double2 *drow = dsm + (size_t)(team * L + (lvl - 1)) * kM;
-        fwd_fft(x, drow, t, bar_team);  // the row's own spectrum buffer is the exchange buffer
+        SZ_FWD(x, drow, t, bar_team);  // the row's own spectrum buffer is the exchange buffer
         team_sync(bar_team);
 #pragma unroll
         for (int sl = 0; sl < 16; sl++) drow[sl * 64 + t] = x[sl];
@@ -460,7 +617,7 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
               for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], dd[q], g[q]);
             }
           }
-          inv_fft(y, tbuf, t, bar_team);
+          SZ_INV(y, tbuf, t, bar_team);
 #pragma unroll
           for (int m = 0; m < 16; m++) {
             accr[m][0] += limb_to_torus(y[m].x, p, P, w);
@@ -487,6 +644,173 @@ __global__ void __launch_bounds__(128 * kMaxCPB, SZ_BR_MINBLOCKS) blind_rotate_k
       }
     __syncthreads();  // abar reuse
   }
+#if SZ_TW_TMEM
+  tmem_fence_before();
+  __syncthreads();
+  if (wid == 0) tmem_dealloc(tmem_slot, 64);
+#endif
+#undef SZ_FWD
+#undef SZ_INV
+}
+
+
+__host__ __device__ constexpr size_t br3_smem_per_ct(int n) {
+  return 2 * kM * sizeof(double2) + ((size_t)n * sizeof(unsigned short) + 15) / 16 * 16;
+}
+
+template <int P>
+__global__ void __launch_bounds__(256, 1) blind_rotate_tmem_kernel(BRArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_all[];
+  __shared__ uint32_t tmem_slot;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = wid >> 2, cs = (wid >> 1) & 1, h = wid & 1;
+  const int t = h * 32 + lane;             // FFT thread index within the team
+  const int ti = g * 64 + t;               // index within the ciphertext's 128 threads
+  const int team = cs * 2 + g;             // team_sync id 1 + team, 64 threads
+  const int pair_id = 5 + cs;              // both teams of this ciphertext, 128 threads
+  const int n = A.n, w = A.w, blog = A.base_log;
+  unsigned char *sm = smem_all + cs * br3_smem_per_ct(n);
+  double2 *tbuf = reinterpret_cast<double2 *>(sm) + g * kM;
+  u64 *accs = reinterpret_cast<u64 *>(tbuf);
+  unsigned short *abar = reinterpret_cast<unsigned short *>(sm + 2 * kM * sizeof(double2));
+
+  if (wid == 0) tmem_alloc(&tmem_slot, kTmCols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tlane = tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16);
+  const uint32_t ta_tw = tlane + kColTw, ta_d0 = tlane + kColD, ta_d1 = tlane + kColD + 64;
+  if (g == 0) {  // pass-1 twiddles of this lane's t, in register order r (k = bitrev4(r))
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      double2 v[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) v[q] = g_tables.tw1[bitrev4(4 * j + q) * 64 + t];
+      uint32_t r16[16];
+      pack4(v, r16);
+      tmem_st16(ta_tw + 16 * j, r16);
+    }
+    tmem_wait_st();
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+
+  const long ngroups = (A.count + 1) / 2;
+  for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const long c = grp * 2 + cs;
+    const bool live = c < A.count;
+    const u64 *lwe = A.lwe_small + (size_t)(live ? c : 0) * (n + 1);
+    for (int i = ti; i < n; i += 128) abar[i] = live ? (unsigned short)sz_modswitch(lwe[i], kLog2_2N) : 0;
+    const int bt = live ? (int)sz_modswitch(lwe[n], kLog2_2N) : 0;
+    u32 id = (A.lut_ids && live) ? A.lut_ids[c] : 0u;
+    if (id >= A.num_luts) id = 0;
+    const u64 *v = A.luts + (size_t)id * kN;
+    u64 accr[16][2];
+#pragma unroll
+    for (int m = 0; m < 16; m++)
+#pragma unroll
+      for (int hh = 0; hh < 2; hh++) {
+        const int j = t + 64 * m + 1024 * hh;
+        const int idx = (j + bt) & (2 * kN - 1);
+        const u64 vv = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
+        accr[m][hh] = g ? vv : 0ull;
+      }
+    bar_sync(pair_id, 128);  // abar visible to both teams
+    for (int i = 0; i < n; i++) {
+      const int a = abar[i];
+#pragma unroll
+      for (int m = 0; m < 16; m++)
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) accs[t + 64 * m + 1024 * hh] = accr[m][hh];
+      team_sync(team);
+      double2 x[16];
+#pragma unroll
+      for (int m = 0; m < 16; m++) {
+        double dv[2];
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+          const int j = t + 64 * m + 1024 * hh;
+          const int src = (j - a) & (2 * kN - 1);
+          const u64 rv = accs[src & (kN - 1)];
+          const u64 rot = (src < kN) ? rv : (u64)0 - rv;
+          u64 r = sz_decomp_round(rot - accr[m][hh], blog, 1);
+          dv[hh] = (double)sz_decomp_next(r, blog);
+        }
+        x[m] = make_double2(dv[0], dv[1]);
+      }
+      fwd_fft_tm(x, tbuf, t, team, ta_tw);
+      {
+        const uint32_t ta_dg = g ? ta_d1 : ta_d0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          uint32_t r16[16];
+          pack4(&x[4 * j], r16);
+          tmem_st16(ta_dg + 16 * j, r16);
+        }
+        tmem_wait_st();
+      }
+      tmem_fence_before();
+      bar_sync(pair_id, 128);
+      tmem_fence_after();
+      // ---------------- inverse: output component o = g, limbs top -> 0
+      const double2 *Gi = A.fbsk + ((size_t)i * 2 + g) * 2 * P * kM;
+#pragma unroll 1
+      for (int p = P - 1; p >= 0; p--) {
+        double2 y[16];
+        const double2 *G0 = Gi + ((size_t)0 * P + p) * kM + t;
+        const double2 *G1 = Gi + ((size_t)1 * P + p) * kM + t;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+          double2 g0[4], g1[4];
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            g0[q] = __ldg(&G0[(4 * j + q) * 64]);
+            g1[q] = __ldg(&G1[(4 * j + q) * 64]);
+          }
+          uint32_t d0[16], d1[16];
+          tmem_ld16(ta_d0 + 16 * j, d0);
+          tmem_ld16(ta_d1 + 16 * j, d1);
+          tmem_wait_ld16x2(d0, d1);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, unpack1(d0, q), g0[q]);
+            cmac(acc, unpack1(d1, q), g1[q]);
+            y[4 * j + q] = acc;
+          }
+        }
+        inv_fft_tm(y, tbuf, t, team, ta_tw);
+#pragma unroll
+        for (int m = 0; m < 16; m++) {
+          accr[m][0] += limb_to_torus(y[m].x, p, P, w);
+          accr[m][1] += limb_to_torus(y[m].y, p, P, w);
+        }
+      }
+      tmem_fence_before();
+      bar_sync(pair_id, 128);  // both teams done reading D^ (TMEM) before the next CMux writes it
+      tmem_fence_after();
+    }
+    if (live) {
+      u64 *out = A.lwe_out + (size_t)c * (kN + 1);
+#pragma unroll
+      for (int m = 0; m < 16; m++)
+#pragma unroll
+        for (int hh = 0; hh < 2; hh++) {
+          const int j = t + 64 * m + 1024 * hh;
+          if (g == 0) {
+            if (j == 0) out[0] = accr[m][hh];
+            else out[kN - j] = (u64)0 - accr[m][hh];
+          } else if (j == 0) {
+            out[kN] = accr[m][hh];
+          }
+        }
+    }
+    bar_sync(pair_id, 128);  // abar reuse
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (wid == 0) tmem_dealloc(tmem_slot, kTmCols);
 }
 
 // --------------------------------------------------------- BSK -> Fourier
@@ -558,7 +882,41 @@ static int plan_blind_rotate(const silenzio_params *P, BRPlan *plan) {
   return SILENZIO_OK;
 }
 
+static int launch_blind_rotate_tmem(const BRArgs &A, const silenzio_params *P, size_t count, cudaStream_t stream) {
+  void (*kern)(BRArgs) = nullptr;
+  if (P->fft_limbs == 1) kern = blind_rotate_tmem_kernel<1>;
+  if (P->fft_limbs == 2) kern = blind_rotate_tmem_kernel<2>;
+  if (P->fft_limbs == 3) kern = blind_rotate_tmem_kernel<3>;
+  if (!kern) return SILENZIO_ERR_UNSUPPORTED;
+  const size_t smem = 2 * br3_smem_per_ct(A.n);
+  if (smem > 200 * 1024) return SILENZIO_ERR_UNSUPPORTED;
+  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int dev = 0, sms = 0;
+  SZ_CUDA_OK(cudaGetDevice(&dev));
+  SZ_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const long wave = 2L * sms;  // one CTA (two ciphertexts) per SM
+  for (long c0 = 0; c0 < (long)count; c0 += wave) {
+    BRArgs W = A;
+    const long cnt = ((long)count - c0 < wave) ? (long)count - c0 : wave;
+    W.lwe_small = A.lwe_small + (size_t)c0 * (A.n + 1);
+    W.lut_ids = A.lut_ids ? A.lut_ids + c0 : nullptr;
+    W.lwe_out = A.lwe_out + (size_t)c0 * (kN + 1);
+    W.count = cnt;
+    kern<<<(unsigned)((cnt + 1) / 2), 256, smem, stream>>>(W);
+    SZ_LAUNCH_OK();
+  }
+  return SILENZIO_OK;
+}
+
 long blind_rotate_wave(const silenzio_params *P) {
+#if SZ_V3
+  if (P->pbs_level == 1) {
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+    return 2L * sms;
+  }
+#endif
   BRPlan plan;
   if (ensure_tables() != SILENZIO_OK || plan_blind_rotate(P, &plan) != SILENZIO_OK) return -1;
   return plan.wave;
@@ -582,6 +940,9 @@ int launch_blind_rotate(const u64 *lwe_small, const u32 *lut_ids, const u64 *lut
   A.base_log = (int)P->pbs_base_log;
   A.P = (int)P->fft_limbs;
   A.w = (int)P->limb_bits;
+#if SZ_V3
+  if (P->pbs_level == 1) return launch_blind_rotate_tmem(A, P, count, stream);
+#endif
   BRPlan plan;
   if ((st = plan_blind_rotate(P, &plan))) return st;
   void (*kern)(BRArgs) = plan.kern;

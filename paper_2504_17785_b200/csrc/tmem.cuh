@@ -1,0 +1,79 @@
+// tmem.cuh -- tensor-memory (TMEM) helpers for sm_100a.
+//
+// TMEM is 128 lanes x 512 columns of 32-bit cells per SM; warp w of a CTA may
+// only access lanes 32 (w % 4) .. 32 (w % 4) + 31, and each thread reads and
+// writes its own lane (shape 32x32b). Measured on B200 (tools/microbench/tmem.cu):
+// tcgen05.ld ~255 B/clk/SM with two loads in flight, tcgen05.st 75-118 B/clk/SM,
+// on a datapath separate from L1/shared memory.
+//
+// Loads are asynchronous: the registers are only valid after tcgen05.wait::ld.
+// The wait helpers below take the loaded registers as in/out operands so the
+// compiler cannot schedule any use of them before the wait.
+#pragma once
+#include <cstdint>
+
+namespace sz {
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// one warp allocates `ncols` (power of two >= 32) columns; address written to *slot
+__device__ __forceinline__ void tmem_alloc(uint32_t *slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tmem_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// 16 x 32-bit cells of this thread's lane, columns [col, col + 16)
+__device__ __forceinline__ void tmem_ld16(uint32_t ta, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta));
+}
+__device__ __forceinline__ void tmem_wait_ld16(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15])::"memory");
+}
+__device__ __forceinline__ void tmem_wait_ld16x2(uint32_t (&r)[16], uint32_t (&q)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]), "+r"(q[0]), "+r"(q[1]), "+r"(q[2]), "+r"(q[3]), "+r"(q[4]), "+r"(q[5]), "+r"(q[6]),
+                 "+r"(q[7]), "+r"(q[8]), "+r"(q[9]), "+r"(q[10]), "+r"(q[11]), "+r"(q[12]), "+r"(q[13]),
+                 "+r"(q[14]), "+r"(q[15])::"memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t ta, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+
+// 4 complex doubles <-> 16 cells (lo word first)
+__device__ __forceinline__ void pack4(const double2 *v, uint32_t (&r)[16]) {
+#pragma unroll
+  for (int i = 0; i < 4; i++) {
+    const unsigned long long a = (unsigned long long)__double_as_longlong(v[i].x);
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[i].y);
+    r[4 * i + 0] = (uint32_t)a;
+    r[4 * i + 1] = (uint32_t)(a >> 32);
+    r[4 * i + 2] = (uint32_t)b;
+    r[4 * i + 3] = (uint32_t)(b >> 32);
+  }
+}
+__device__ __forceinline__ double2 unpack1(const uint32_t (&r)[16], int i) {
+  const unsigned long long a = ((unsigned long long)r[4 * i + 1] << 32) | r[4 * i + 0];
+  const unsigned long long b = ((unsigned long long)r[4 * i + 3] << 32) | r[4 * i + 2];
+  return make_double2(__longlong_as_double((long long)a), __longlong_as_double((long long)b));
+}
+
+}  // namespace sz
