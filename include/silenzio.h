@@ -162,6 +162,38 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
                         const uint64_t *ksk, const silenzio_params *params, void *workspace,
                         size_t workspace_bytes, void *stream);
 
+/* Config-4 gadgets at parameter set A (DESIGN.md §Config 4). Each call composes
+ * linear LWE ops and PBS only. Ciphertext arrays are big-key LWE [*][kN+1];
+ * residues / digits / bits are encoded at Delta = 2^59; `moduli_host` must be
+ * ascending with every m <= 16 (SILENZIO_ERR_WINDOW otherwise); workspace >=
+ * silenzio_gadget_workspace_bytes(params, k, count). Calls synchronise `stream`.
+ *  silenzio_rns2mrns        Alg. 1 RNS2MRNS: in [k][count]
+ *                           residues -> out [k][count] MRNS digits (least significant first).
+ *  silenzio_rns_sign_abs    Sign_(-1,1,1) via the top MRNS digit >= r_k/2 (l.309-323; r_k even)
+ *                           -> sign_out [count] in {0 (>= 0), 1 (< 0)}; |x| per residue
+ *                           (Alg. 4, l.414-415) -> abs_out [k][count].
+ *  silenzio_mrns_bitlen_max Alg. 3 step 2 (l.344-349): bitlen_out [k][count] = bit length of
+ *                           every digit; max_out [k] = tensor-wide maximum per digit position.
+ *  silenzio_int_ce_grad     Alg. 5 IntCELossDeriv (l.433-450) at Gamma = 4, kappa = 0 (DESIGN
+ *                           R10, R12): Yhat [a][b] signed in [-8,8), Y [a][b] one-hot bits,
+ *                           b <= 13 -> out [a][b] in {-1, 0, 1}. */
+size_t silenzio_gadget_workspace_bytes(const silenzio_params *params, uint32_t k, size_t count);
+int silenzio_rns2mrns(const uint64_t *in, const uint32_t *moduli_host, uint32_t k, size_t count,
+                      uint64_t *out, const void *fourier_bsk, const uint64_t *ksk,
+                      const silenzio_params *params, void *workspace, size_t workspace_bytes,
+                      void *stream);
+int silenzio_rns_sign_abs(const uint64_t *in, const uint32_t *moduli_host, uint32_t k, size_t count,
+                          uint64_t *sign_out, uint64_t *abs_out, const void *fourier_bsk,
+                          const uint64_t *ksk, const silenzio_params *params, void *workspace,
+                          size_t workspace_bytes, void *stream);
+int silenzio_mrns_bitlen_max(const uint64_t *digits, uint32_t k, size_t count, uint64_t *bitlen_out,
+                             uint64_t *max_out, const void *fourier_bsk, const uint64_t *ksk,
+                             const silenzio_params *params, void *workspace, size_t workspace_bytes,
+                             void *stream);
+int silenzio_int_ce_grad(const uint64_t *Yhat, const uint64_t *Y, uint32_t a, uint32_t b, uint64_t *out,
+                         const void *fourier_bsk, const uint64_t *ksk, const silenzio_params *params,
+                         void *workspace, size_t workspace_bytes, void *stream);
+
 /* ------------------------------------- client-side key / ciphertext generation
  * All random numbers are inputs (drawn by the caller), so every key and
  * ciphertext is a deterministic function of the caller's seeded draws. */

@@ -154,3 +154,111 @@ def decode_residues(phases, moduli):
         v = ((np.asarray(ph, dtype=np.uint64) + np.uint64(1 << (d - 1))) >> np.uint64(d)).astype(np.int64)
         out.append(v % (16 if m == 16 else 32) % m)
     return np.stack(out)
+
+
+# ---------------------------------------------------------------- config 4
+# Same schedule as DESIGN.md §Config 4, written independently of
+# paper_2504_17785_b200/csrc/gadgets_mrns.cu. Elementwise linear steps use
+# plain numpy u64 arithmetic (exact mod 2^64).
+HALF_DELTA = 1 << (DELTA_LOG - 1)
+
+
+def table_raw(window_start: int, f) -> np.ndarray:
+    """Like table() but f returns raw torus integers (allows half-step values)."""
+    tab = [0] * 16
+    for x in range(window_start, window_start + 16):
+        xm = x % 32
+        v = _u(f(x))
+        if xm < 16:
+            tab[xm] = v
+        else:
+            tab[xm - 16] = _u(-v)
+    return np.array(tab, dtype=np.uint64)
+
+
+def axpy(terms, cst=0):
+    """sum c * A + (0,..,0,cst) over (c, A) pairs, elementwise (u64 wrap)."""
+    out = None
+    for c, A in terms:
+        v = np.uint64(c % (1 << 64)) * np.asarray(A, dtype=np.uint64)
+        out = v if out is None else out + v
+    out = out.copy()
+    out[..., -1] += np.uint64(_u(cst))
+    return out
+
+
+def rns2mrns_fhe(ctx: Ctx, res, moduli):
+    """Alg. 1 on residue ciphertexts res [k][count] -> digits [k][count]."""
+    y = [np.array(r, dtype=np.uint64) for r in res]
+    for i in range(1, len(moduli)):
+        mp = moduli[i - 1]
+        for j in range(i, len(moduli)):
+            mj = moduli[j]
+            t = pow(mp, -1, mj)
+            d = axpy([(1, y[j]), (-1, y[i - 1])])
+            if mp + mj - 1 <= 16:
+                y[j] = ctx.lut(d, [table(-(mp - 1), lambda v, mj=mj, t=t: (v * t) % mj, DELTA_LOG)])
+            else:
+                half = mj * HALF_DELTA
+                sig = ctx.lut(d, [const_table(half)])
+                u = axpy([(1, d), (-1, sig)], half)
+                y[j] = ctx.lut(u, [table(0, lambda v, mj=mj, t=t: (v * t) % mj, DELTA_LOG)])
+    return np.stack(y)
+
+
+def sign_abs_fhe(ctx: Ctx, res, moduli):
+    """Sign_(-1,1,1) bit (top MRNS digit >= r_k/2) and |x| per residue (Alg. 4)."""
+    digits = rns2mrns_fhe(ctx, res, moduli)
+    rk = moduli[-1]
+    e = ctx.lut(digits[-1], [table(0, lambda y: 1 if 2 * y >= rk else 0, DELTA_LOG)])
+    out = []
+    for j, m in enumerate(moduli):
+        x = res[j]
+        A = ctx.lut(x, [table_raw(0, lambda v, m=m: 0 if v == 0 else m * HALF_DELTA)])
+        q = axpy([(16, e), (1, x)])
+        B = ctx.lut(q, [table_raw(0, lambda v, m=m: 0 if v == 0 else (2 * v - m) * HALF_DELTA)])
+        out.append(axpy([(1, A), (1, B)]))
+    return e, np.stack(out), digits
+
+
+def bitlen_max_fhe(ctx: Ctx, digits):
+    """Alg. 3 step 2: bit length of each digit and the tensor-wide max per position
+    (max tree, first half against second half: max(a,b) = b + ReLU(a - b))."""
+    bl = np.stack([ctx.lut(d, [table(0, lambda v: int(v).bit_length(), DELTA_LOG)]) for d in digits])
+    mx = []
+    for i in range(len(digits)):
+        buf = bl[i].copy()
+        cur = len(buf)
+        while cur > 1:
+            half = cur // 2
+            t = axpy([(1, buf[:half]), (-1, buf[half:2 * half])])
+            r = ctx.lut(t, [table(-8, lambda d: max(d, 0), DELTA_LOG)])
+            newbuf = axpy([(1, buf[half:2 * half]), (1, r)])
+            if cur & 1:
+                newbuf = np.concatenate([newbuf, buf[cur - 1:cur]])
+            buf = newbuf
+            cur = half + (cur & 1)
+        mx.append(buf[0])
+    return bl, np.stack(mx)
+
+
+def int_ce_grad_fhe(ctx: Ctx, Yhat, Y):
+    """Alg. 5 at Gamma = 4, kappa = 0 (R10, R12) on [a][b] ciphertexts."""
+    a, b = Yhat.shape[0], Yhat.shape[1]
+    rhe = lambda v: int(np.rint(v))  # noqa: E731  (half to even)
+    flat = lambda z: z.reshape(a * b, -1)  # noqa: E731
+    E = ctx.lut(flat(Yhat), [table(-8, lambda v: 1 if v == 7 else 0, DELTA_LOG)])
+    S = E.reshape(a, b, -1).sum(axis=1, dtype=np.uint64)
+    Sb = np.repeat(S, b, axis=0)
+    g0 = lambda s: rhe(1.0 / (s + 1))  # noqa: E731
+    g1 = lambda s: rhe(2.0 / (s + 1))  # noqa: E731
+    A = ctx.lut(Sb, [table_raw(0, lambda s: (g0(s) + g1(s)) * HALF_DELTA)])
+    B = ctx.lut(axpy([(16, E), (1, Sb)]), [table_raw(0, lambda s: (g0(s) - g1(s)) * HALF_DELTA)])
+    Ep = axpy([(1, B), (1, A)])
+    R = Ep.reshape(a, b, -1).sum(axis=1, dtype=np.uint64)
+    Rb = np.repeat(R, b, axis=0)
+    A2 = ctx.lut(Rb, [table_raw(0, lambda r: r * HALF_DELTA)])
+    B2 = ctx.lut(axpy([(16, flat(Y)), (1, Rb)]), [table_raw(0, lambda r: -r * HALF_DELTA)])
+    Z = axpy([(1, Ep), (-1, A2), (-1, B2)])
+    out = ctx.lut(Z, [table(-13, lambda v: (v > 0) - (v < 0), DELTA_LOG)])
+    return out.reshape(a, b, -1)

@@ -16,109 +16,10 @@
 //   g3 modular sums     m = 16: native wrap at 2^60; m in {5,7}: clean groups
 //                       of 3 / 2 reduced by a fresh mod-m PBS; m >= 9: pair
 //                       tree of T3 reductions.
-#include <cstring>
-#include <vector>
 
-#include "common.cuh"
+#include "gadget_util.cuh"
 
-extern "C" {
-int silenzio_pbs_batch(const uint64_t *, const uint32_t *, const uint64_t *, uint32_t, const void *,
-                       const uint64_t *, uint64_t *, size_t, const silenzio_params *, void *, void *);
-int silenzio_lwe_linear_batch(const uint64_t *, const uint32_t *, const int64_t *, const uint64_t *, uint32_t,
-                              uint32_t, size_t, uint64_t *, void *);
-int silenzio_build_testpoly(const uint64_t *, uint32_t, uint32_t, uint32_t, uint64_t *, void *);
-size_t silenzio_pbs_workspace_bytes(const silenzio_params *, size_t);
-}
-
-namespace {
-
-constexpr int kP = 4;                   // message bits (set A)
-constexpr u64 kDelta = 1ull << 59;      // 2^(64 - (p+1))
-constexpr u64 kDelta16 = 1ull << 60;    // scale of the native mod-16 channel
-
-u64 enc(i64 v, u64 scale) { return (u64)v * scale; }
-
-int inv4(int m) {
-  for (int x = 1; x < m; x++)
-    if ((4 * x) % m == 1) return x;
-  return -1;
-}
-
-int pmod(long v, int m) { return (int)(((v % m) + m) % m); }
-
-// 16-entry tables of torus values for window [w0, w0 + 16) of Z_32 (SURVEY
-// toolbox T1): T[x mod 16] = f(x) for x in [0,16); inputs x in [16,32) return
-// -T[x - 16], so a negative input x in [-8,0) needs T[x + 16] = -f(x).
-template <class F>
-std::vector<u64> table_window(int w0, F f) {
-  std::vector<u64> T(16, 0);
-  for (int x = w0; x < w0 + 16; x++) {
-    const int xm = ((x % 32) + 32) % 32;
-    if (xm < 16) T[xm] = f(x);
-    else T[xm - 16] = (u64)0 - f(x);
-  }
-  return T;
-}
-
-struct Dev {
-  cudaStream_t st;
-  const silenzio_params *P;
-  const void *fbsk;
-  const u64 *ksk;
-  size_t big;  // k N + 1
-  // scratch
-  u64 *luts;           // [kMaxLuts][N]
-  u64 *tables;         // [kMaxLuts][16]
-  u32 *idx;            // linear-op index scratch
-  i64 *coef;
-  u64 *cst;
-  u32 *ids;            // lut ids
-  void *pbs_ws;
-  size_t idx_cap, ids_cap, pbs_cap;
-};
-
-constexpr int kMaxLuts = 4;
-
-int upload_luts(Dev &D, const std::vector<std::vector<u64>> &tabs) {
-  std::vector<u64> flat;
-  for (auto &t : tabs) flat.insert(flat.end(), t.begin(), t.end());
-  SZ_CUDA_OK(cudaMemcpyAsync(D.tables, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, D.st));
-  return silenzio_build_testpoly(D.tables, (u32)tabs.size(), kP, D.P->poly_size, D.luts, D.st);
-}
-
-// out[i] = sum_t coef[i][t] * in[idx[i][t]] + cst[i]
-int linear(Dev &D, const u64 *in, u64 *out, size_t count, int terms, const std::vector<u32> &idx,
-           const std::vector<i64> &coef, const std::vector<u64> &cst) {
-  if (count == 0) return SILENZIO_OK;
-  if (count * terms > D.idx_cap || count > D.idx_cap) return SILENZIO_ERR_WORKSPACE;
-  SZ_CUDA_OK(cudaMemcpyAsync(D.idx, idx.data(), count * terms * 4, cudaMemcpyHostToDevice, D.st));
-  SZ_CUDA_OK(cudaMemcpyAsync(D.coef, coef.data(), count * terms * 8, cudaMemcpyHostToDevice, D.st));
-  SZ_CUDA_OK(cudaMemcpyAsync(D.cst, cst.data(), count * 8, cudaMemcpyHostToDevice, D.st));
-  // the staging buffers are reused by the next call: keep host vectors alive
-  // until the copies have been consumed
-  SZ_CUDA_OK(cudaStreamSynchronize(D.st));
-  return silenzio_lwe_linear_batch(in, D.idx, D.coef, D.cst, (u32)terms, (u32)(D.big - 1), count, out, D.st);
-}
-
-// PBS of `count` ciphertexts; lut id per ciphertext (empty = all 0)
-int lookup(Dev &D, const u64 *in, u64 *out, size_t count, const std::vector<u32> &ids, u32 num_luts) {
-  if (count == 0) return SILENZIO_OK;
-  const size_t chunk = D.pbs_cap;
-  for (size_t c0 = 0; c0 < count; c0 += chunk) {
-    const size_t cnt = count - c0 < chunk ? count - c0 : chunk;
-    const u32 *idp = nullptr;
-    if (!ids.empty()) {
-      if (cnt > D.ids_cap) return SILENZIO_ERR_WORKSPACE;
-      SZ_CUDA_OK(cudaMemcpyAsync(D.ids, ids.data() + c0, cnt * 4, cudaMemcpyHostToDevice, D.st));
-      SZ_CUDA_OK(cudaStreamSynchronize(D.st));
-      idp = D.ids;
-    }
-    int rc = silenzio_pbs_batch(in + c0 * D.big, idp, D.luts, num_luts, D.fbsk, D.ksk, out + c0 * D.big, cnt, D.P,
-                                D.pbs_ws, D.st);
-    if (rc) return rc;
-  }
-  return SILENZIO_OK;
-}
+namespace szg {
 
 // Pairwise/grouped reduction tree over `groups` independent groups of `terms`
 // consecutive ciphertexts in buf (in place). Returns the group results in
@@ -191,7 +92,9 @@ int sum_tree(Dev &D, int m, u64 *buf, u64 *tmp, u64 *tmp2, size_t groups, size_t
   return SILENZIO_OK;
 }
 
-}  // namespace
+}  // namespace szg
+
+using namespace szg;
 
 extern "C" {
 

@@ -137,6 +137,20 @@ __global__ void lwe_linear_kernel(const u64 *in, const u32 *idx, const i64 *coef
   }
 }
 
+// out[e] = ca A[e] + cb B[e] + cc C[e] + (0,...,0,cst)   (elementwise, exact mod 2^64)
+__global__ void lwe_axpy3_kernel(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc,
+                                 u64 cst, long count, int dim) {
+  const long total = count * (long)(dim + 1);
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    u64 s = 0;
+    if (A) s += (u64)ca * A[e];
+    if (B) s += (u64)cb * B[e];
+    if (C) s += (u64)cc * C[e];
+    if (e % (dim + 1) == dim) s += cst;
+    out[e] = s;
+  }
+}
+
 // ------------------------------------------------------------ host launch
 int launch_lwe_encrypt(const u64 *mask, const i64 *noise, const u64 *pt, const u64 *key, int dim,
                        size_t count, u64 *out, cudaStream_t st) {
@@ -177,6 +191,17 @@ int launch_ksk_generate(const u64 *in_key, const u64 *lwe_key, const u64 *mask, 
 int launch_testpoly(const u64 *tables, int num, int p, int N, u64 *polys, cudaStream_t st) {
   const long total = (long)num * N;
   testpoly_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(tables, num, p, N, polys);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+int launch_lwe_axpy3(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc, u64 cst,
+                     size_t count, int dim, cudaStream_t st) {
+  if (count == 0) return SILENZIO_OK;
+  const long total = (long)count * (dim + 1);
+  long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  lwe_axpy3_kernel<<<(unsigned)blocks, 256, 0, st>>>(out, A, ca, B, cb, C, cc, cst, (long)count, dim);
   SZ_LAUNCH_OK();
   return SILENZIO_OK;
 }

@@ -57,6 +57,11 @@ def load():
         "silenzio_ksk_generate": ([V, V, V, V, V, U32, U32, U32, U32, V], I),
         "silenzio_rns_matmul_workspace_bytes": ([P, U32, U32, U32], S),
         "silenzio_rns_matmul": ([V, V, U32, U32, U32, V, U32, V, V, V, P, V, S, V], I),
+        "silenzio_gadget_workspace_bytes": ([P, U32, S], S),
+        "silenzio_rns2mrns": ([V, V, U32, S, V, V, V, P, V, S, V], I),
+        "silenzio_rns_sign_abs": ([V, V, U32, S, V, V, V, V, P, V, S, V], I),
+        "silenzio_mrns_bitlen_max": ([V, U32, S, V, V, V, V, P, V, S, V], I),
+        "silenzio_int_ce_grad": ([V, V, U32, U32, V, V, V, P, V, S, V], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -74,7 +79,8 @@ def exported_symbols():
         "silenzio_blind_rotate_batch", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
         "silenzio_build_testpoly", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
         "silenzio_bsk_generate", "silenzio_ksk_generate", "silenzio_rns_matmul_workspace_bytes",
-        "silenzio_rns_matmul",
+        "silenzio_rns_matmul", "silenzio_gadget_workspace_bytes", "silenzio_rns2mrns",
+        "silenzio_rns_sign_abs", "silenzio_mrns_bitlen_max", "silenzio_int_ce_grad",
     ]
 
 
@@ -265,4 +271,57 @@ def rns_matmul(X, W, moduli, fourier_bsk, ksk, P, out=None, workspace=None, stre
     _check(load().silenzio_rns_matmul(_ptr(X), _ptr(W), a, b, c, mod_arr, k, _ptr(out), _ptr(fourier_bsk),
                                       _ptr(ksk), ctypes.byref(make_params(P)), _ptr(workspace),
                                       workspace.numel(), _stream(stream)))
+    return out
+
+
+def _gws(P, k, count, device):
+    n = load().silenzio_gadget_workspace_bytes(ctypes.byref(make_params(P)), k, count)
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def _moduli(moduli):
+    return (ctypes.c_uint32 * len(moduli))(*[int(m) for m in moduli])
+
+
+def rns2mrns(residues, moduli, fourier_bsk, ksk, P, stream=None):
+    """residues [k][count] ciphertexts -> MRNS digits [k][count] (Alg. 1)."""
+    k, count = int(residues.shape[0]), int(residues.shape[1])
+    out = torch.empty_like(residues)
+    ws = _gws(P, k, count, residues.device)
+    _check(load().silenzio_rns2mrns(_ptr(residues), _moduli(moduli), k, count, _ptr(out), _ptr(fourier_bsk),
+                                    _ptr(ksk), ctypes.byref(make_params(P)), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def rns_sign_abs(residues, moduli, fourier_bsk, ksk, P, stream=None):
+    """residues [k][count] -> (sign bits [count], |x| residues [k][count])."""
+    k, count = int(residues.shape[0]), int(residues.shape[1])
+    sign = torch.empty((count, residues.shape[-1]), dtype=torch.int64, device=residues.device)
+    absr = torch.empty_like(residues)
+    ws = _gws(P, k, count, residues.device)
+    _check(load().silenzio_rns_sign_abs(_ptr(residues), _moduli(moduli), k, count, _ptr(sign), _ptr(absr),
+                                        _ptr(fourier_bsk), _ptr(ksk), ctypes.byref(make_params(P)), _ptr(ws),
+                                        ws.numel(), _stream(stream)))
+    return sign, absr
+
+
+def mrns_bitlen_max(digits, fourier_bsk, ksk, P, stream=None):
+    """MRNS digits [k][count] -> (bit lengths [k][count], tensor-wide max per position [k])."""
+    k, count = int(digits.shape[0]), int(digits.shape[1])
+    bl = torch.empty_like(digits)
+    mx = torch.empty((k, digits.shape[-1]), dtype=torch.int64, device=digits.device)
+    ws = _gws(P, k, count, digits.device)
+    _check(load().silenzio_mrns_bitlen_max(_ptr(digits), k, count, _ptr(bl), _ptr(mx), _ptr(fourier_bsk),
+                                           _ptr(ksk), ctypes.byref(make_params(P)), _ptr(ws), ws.numel(),
+                                           _stream(stream)))
+    return bl, mx
+
+
+def int_ce_grad(Yhat, Y, fourier_bsk, ksk, P, stream=None):
+    """Yhat [a][b] signed logits, Y [a][b] one-hot bits -> error signs [a][b] (Alg. 5)."""
+    a, b = int(Yhat.shape[0]), int(Yhat.shape[1])
+    out = torch.empty_like(Yhat)
+    ws = _gws(P, 1, a * b, Yhat.device)
+    _check(load().silenzio_int_ce_grad(_ptr(Yhat), _ptr(Y), a, b, _ptr(out), _ptr(fourier_bsk), _ptr(ksk),
+                                       ctypes.byref(make_params(P)), _ptr(ws), ws.numel(), _stream(stream)))
     return out

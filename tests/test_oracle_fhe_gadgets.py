@@ -56,3 +56,51 @@ def test_schedule_tables_realise_their_functions_on_the_window():
         for w in range(16):
             a0, a1, b0, b1 = x & 3, x >> 2, w & 3, w >> 2
             assert (a0 * b0 + 4 * a0 * b1 + 4 * a1 * b0) % 16 == (x * w) % 16
+
+
+BASE6 = [5, 7, 9, 11, 13, 16]
+
+
+def encrypt_residues(P, K, vals, moduli, seed):
+    """Residues of signed ints, each encrypted at Delta: [k][count] ciphertexts."""
+    res = G.to_rns(np.asarray(vals), moduli)
+    return np.stack([encrypt_ints(P, K, r, seed + i) for i, r in enumerate(res)])
+
+
+def test_config4_set_a_gadgets_fhe_tiny():
+    """RNS2MRNS (Alg. 1), sign/abs (Alg. 4 step 1-2), bit length + block max
+    (Alg. 3 step 2) through the oracle's encrypted composition."""
+    P = get_params("A_SMALLN")
+    K = oracle.keygen(P, key_randomness(P, 51))
+    M = math.prod(BASE6)
+    x = np.array([-50176, -7, 0, 611, 360359, -360360]) % M
+    x = G.signed_decode(x, M)
+    ctx = F.Ctx(P, K)
+    res_ct = encrypt_residues(P, K, x, BASE6, 10)
+    dec = lambda c: oracle.decode(oracle.lwe_phase(c, K["big_key"]), P.p)  # noqa: E731
+    digits = F.rns2mrns_fhe(ctx, res_ct, BASE6)
+    ref_digits, _ = G.rns2mrns(G.to_rns(x, BASE6), BASE6)
+    assert np.array_equal(dec(digits), ref_digits)
+    e, absr, _ = F.sign_abs_fhe(ctx, res_ct, BASE6)
+    assert np.array_equal(dec(e), (G.sign_rns(G.to_rns(x, BASE6), BASE6) < 0).astype(np.int64))
+    assert np.array_equal(dec(absr), G.to_rns(np.abs(x), BASE6))
+    bl, mx = F.bitlen_max_fhe(ctx, digits)
+    ref_bl = np.stack([[int(v).bit_length() for v in row] for row in ref_digits])
+    assert np.array_equal(dec(bl), ref_bl)
+    assert np.array_equal(dec(mx), ref_bl.max(axis=1))
+
+
+def test_int_ce_grad_fhe_tiny():
+    P = get_params("A_SMALLN")
+    K = oracle.keygen(P, key_randomness(P, 52))
+    rng = np.random.default_rng(52)
+    Yhat = rng.integers(-8, 8, size=(2, 10))
+    Yhat[0, 3] = 7
+    Yhat[1, [1, 4]] = 7
+    Y = np.zeros((2, 10), dtype=np.int64)
+    Y[0, 3] = 1
+    Y[1, 6] = 1
+    ctx = F.Ctx(P, K)
+    out = F.int_ce_grad_fhe(ctx, encrypt_ints(P, K, Yhat, 1), encrypt_ints(P, K, Y, 2))
+    got = G.signed_decode(oracle.decode(oracle.lwe_phase(out, K["big_key"]), P.p), 32)
+    assert np.array_equal(got, G.int_ce_loss_deriv(Yhat, Y, gamma=3, kappa=0))
