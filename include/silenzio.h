@@ -69,7 +69,8 @@ const char *silenzio_version(void);
 /* Bytes of the Fourier-domain bootstrapping key: n*(k+1)l*(k+1)*P*(N/2)*16. */
 size_t silenzio_fourier_bsk_bytes(const silenzio_params *params);
 /* Bytes of workspace silenzio_pbs_batch needs for `count` ciphertexts
- * (the keyswitched small-key LWEs, count*(n+1)*8, rounded up). */
+ * (the keyswitched small-key LWEs, count*(n+1)*8, rounded up, plus the
+ * blind-rotation workspace). */
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *params, size_t count);
 
 /* Number of kernel launches silenzio_pbs_batch makes for `count` ciphertexts:
@@ -111,11 +112,16 @@ int silenzio_pbs_batch(const uint64_t *lwe_in, const uint32_t *lut_ids, const ui
 
 /* Blind rotation + sample extraction only (MS -> BR -> SE) of small-key
  * inputs [count][n+1]; output [count][kN+1]. Used to check the stages
- * separately against the oracle and for the literal MS->BR->SE->KS order. */
+ * separately against the oracle, for the literal MS->BR->SE->KS order and for
+ * cross-parameter pipelines (set B). `workspace` must hold
+ * silenzio_blind_rotate_workspace_bytes(params, count) bytes (0 for N <= 8192,
+ * where it may be NULL; N = 32768 keeps each in-flight ciphertext's accumulator
+ * and spectra there, 1.75 MiB per ciphertext, at most 48 in flight). */
+size_t silenzio_blind_rotate_workspace_bytes(const silenzio_params *params, size_t count);
 int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_ids,
                                 const uint64_t *luts, uint32_t num_luts, const void *fourier_bsk,
                                 uint64_t *lwe_out, size_t count, const silenzio_params *params,
-                                void *stream);
+                                void *workspace, void *stream);
 
 /* Same as silenzio_pbs_batch but lwe_in / lwe_out are HOST buffers (pinned
  * memory recommended). Copies are chunked (`chunk` ciphertexts, 0 = auto) and
@@ -205,10 +211,13 @@ int silenzio_lwe_encrypt_batch(const uint64_t *mask, const int64_t *noise,
 int silenzio_lwe_phase_batch(const uint64_t *ct, const uint64_t *key, uint32_t dim, size_t count,
                              uint64_t *phase, void *stream);
 /* GGSW bootstrapping key (C6): mask [n][(k+1)l][k][N], noise [n][(k+1)l][N],
- * lwe_key [n] in {0,1}, glwe_key [k][N] in {0,1} -> bsk [n][(k+1)l][k+1][N]. */
+ * lwe_key [n] in {0,1}, glwe_key [k][N] in {0,1} -> bsk [n][(k+1)l][k+1][N].
+ * N = 32768 computes the GLWE bodies with an exact limb-split FFT and needs
+ * silenzio_bsk_generate_workspace_bytes() of workspace (0 otherwise; NULL ok). */
+size_t silenzio_bsk_generate_workspace_bytes(const silenzio_params *params);
 int silenzio_bsk_generate(const uint64_t *lwe_key, const uint64_t *glwe_key, const uint64_t *mask,
                           const int64_t *noise, uint64_t *bsk, const silenzio_params *params,
-                          void *stream);
+                          void *workspace, void *stream);
 /* Keyswitching key (C3): KSK[j][t] = LWE_s(s_in[j] * 2^{64 - t*base_log}),
  * mask [in_dim][level][n], noise [in_dim][level] -> ksk [in_dim][level][n+1]. */
 int silenzio_ksk_generate(const uint64_t *in_key, const uint64_t *lwe_key, const uint64_t *mask,

@@ -14,11 +14,19 @@ int launch_blind_rotate_large(const u64 *, const u32 *, const u64 *, u32, const 
                               const silenzio_params *, cudaStream_t);
 int launch_bsk_to_fourier_large(const u64 *, void *, const silenzio_params *, cudaStream_t);
 long blind_rotate_large_wave(const silenzio_params *);
+int launch_blind_rotate_huge(const u64 *, const u32 *, const u64 *, u32, const void *, u64 *, size_t,
+                             const silenzio_params *, void *, cudaStream_t);
+int launch_bsk_to_fourier_huge(const u64 *, void *, const silenzio_params *, cudaStream_t);
+size_t blind_rotate_huge_ws_bytes(const silenzio_params *, size_t);
+long blind_rotate_huge_wave(const silenzio_params *);
 int launch_keyswitch(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, cudaStream_t);
 int launch_lwe_encrypt(const u64 *, const i64 *, const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_lwe_phase(const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_bsk_generate(const u64 *, const u64 *, const u64 *, const i64 *, u64 *, int, int, int, int, int,
                         cudaStream_t);
+int launch_bsk_generate_huge(const u64 *, const u64 *, const u64 *, const i64 *, u64 *, int, int, int, int, void *,
+                             cudaStream_t);
+size_t glwe_body_huge_ws_bytes();
 int launch_ksk_generate(const u64 *, const u64 *, const u64 *, const i64 *, u64 *, int, int, int, int,
                         cudaStream_t);
 int launch_testpoly(const u64 *, int, int, int, u64 *, cudaStream_t);
@@ -58,6 +66,11 @@ int check_br_supported(const silenzio_params *P) {
     if (P->pbs_level > 4 || P->lwe_dim > 4096) return SILENZIO_ERR_UNSUPPORTED;
     return SILENZIO_OK;
   }
+  if (P->poly_size == 32768) {
+    if (!(P->pbs_level == 1 || P->pbs_level == 2 || P->pbs_level == 4) || P->fft_limbs != 3 || P->lwe_dim > 8192)
+      return SILENZIO_ERR_UNSUPPORTED;
+    return SILENZIO_OK;
+  }
   return SILENZIO_ERR_UNSUPPORTED;
 }
 
@@ -68,7 +81,7 @@ int check_ks_params(const silenzio_params *P) {
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-const char *kVersion = "libsilenzio 0.2 (sm_100a; blind rotation N=2048 and N=8192; P-limb exact FFT)";
+const char *kVersion = "libsilenzio 0.3 (sm_100a; blind rotation N=2048, 8192, 32768; P-limb exact FFT)";
 
 }  // namespace
 
@@ -97,9 +110,15 @@ size_t silenzio_fourier_bsk_bytes(const silenzio_params *P) {
   return (size_t)P->lwe_dim * rows * (P->glwe_dim + 1) * P->fft_limbs * (P->poly_size / 2) * 16;
 }
 
+size_t silenzio_blind_rotate_workspace_bytes(const silenzio_params *P, size_t count) {
+  if (check_params(P) != SILENZIO_OK) return 0;
+  if (P->poly_size == 32768) return round_up(blind_rotate_huge_ws_bytes(P, count), 256);
+  return 0;
+}
+
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *P, size_t count) {
   if (check_params(P) != SILENZIO_OK) return 0;
-  return round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256);
+  return round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256) + silenzio_blind_rotate_workspace_bytes(P, count);
 }
 
 int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fbsk, const silenzio_params *P, void *stream) {
@@ -109,6 +128,7 @@ int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fbsk, const silenzio_para
   if (!sz_aligned16(bsk) || !sz_aligned16(fbsk)) return SILENZIO_ERR_MISALIGNED;
   if ((st = check_br_supported(P))) return st;
   if (P->poly_size == 8192) return launch_bsk_to_fourier_large(bsk, fbsk, P, sz_stream(stream));
+  if (P->poly_size == 32768) return launch_bsk_to_fourier_huge(bsk, fbsk, P, sz_stream(stream));
   return launch_bsk_to_fourier(bsk, fbsk, P, sz_stream(stream));
 }
 
@@ -126,7 +146,7 @@ int silenzio_keyswitch_batch(const uint64_t *in, const uint64_t *ksk, uint64_t *
 
 int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_ids, const uint64_t *luts,
                                 uint32_t num_luts, const void *fbsk, uint64_t *out, size_t count,
-                                const silenzio_params *P, void *stream) {
+                                const silenzio_params *P, void *workspace, void *stream) {
   int st = check_params(P);
   if (st) return st;
   if ((st = check_br_supported(P))) return st;
@@ -137,6 +157,9 @@ int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_i
   if (count > (1ull << 31)) return SILENZIO_ERR_COUNT;
   if (P->poly_size == 8192)
     return launch_blind_rotate_large(lwe_small, lut_ids, luts, num_luts, fbsk, out, count, P, sz_stream(stream));
+  if (P->poly_size == 32768)
+    return launch_blind_rotate_huge(lwe_small, lut_ids, luts, num_luts, fbsk, out, count, P, workspace,
+                                    sz_stream(stream));
   return launch_blind_rotate(lwe_small, lut_ids, luts, num_luts, fbsk, out, count, P, sz_stream(stream));
 }
 
@@ -156,13 +179,16 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
   if ((st = launch_keyswitch(in, ksk, small, count, (int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_base_log,
                              (int)P->ks_level, sz_stream(stream))))
     return st;
-  return silenzio_blind_rotate_batch(small, lut_ids, luts, num_luts, fbsk, out, count, P, stream);
+  void *br_ws = reinterpret_cast<unsigned char *>(workspace) + round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256);
+  return silenzio_blind_rotate_batch(small, lut_ids, luts, num_luts, fbsk, out, count, P, br_ws, stream);
 }
 
 long silenzio_pbs_launch_count(const silenzio_params *P, size_t count) {
   if (check_params(P) != SILENZIO_OK || check_br_supported(P) != SILENZIO_OK) return -1;
   if (count == 0) return 0;
-  const long wave = P->poly_size == 8192 ? blind_rotate_large_wave(P) : blind_rotate_wave(P);
+  const long wave = P->poly_size == 8192    ? blind_rotate_large_wave(P)
+                   : P->poly_size == 32768 ? blind_rotate_huge_wave(P)
+                                           : blind_rotate_wave(P);
   if (wave <= 0) return -1;
   return 1 + (long)((count + wave - 1) / wave);  // keyswitch + one blind rotation per wave
 }
@@ -262,11 +288,23 @@ int silenzio_lwe_phase_batch(const uint64_t *ct, const uint64_t *key, uint32_t d
   return launch_lwe_phase(ct, key, (int)dim, count, phase, sz_stream(stream));
 }
 
+size_t silenzio_bsk_generate_workspace_bytes(const silenzio_params *P) {
+  if (check_params(P) != SILENZIO_OK) return 0;
+  return P->poly_size == 32768 ? glwe_body_huge_ws_bytes() : 0;
+}
+
 int silenzio_bsk_generate(const uint64_t *lwe_key, const uint64_t *glwe_key, const uint64_t *mask,
-                          const int64_t *noise, uint64_t *bsk, const silenzio_params *P, void *stream) {
+                          const int64_t *noise, uint64_t *bsk, const silenzio_params *P, void *workspace,
+                          void *stream) {
   int st = check_params(P);
   if (st) return st;
   if (!lwe_key || !glwe_key || !mask || !noise || !bsk) return SILENZIO_ERR_NULL_POINTER;
+  if (P->poly_size == 32768) {
+    if (P->glwe_dim != 1) return SILENZIO_ERR_UNSUPPORTED;
+    return launch_bsk_generate_huge(lwe_key, glwe_key, mask, reinterpret_cast<const i64 *>(noise), bsk,
+                                    (int)P->lwe_dim, (int)P->poly_size, (int)P->pbs_base_log, (int)P->pbs_level,
+                                    workspace, sz_stream(stream));
+  }
   return launch_bsk_generate(lwe_key, glwe_key, mask, reinterpret_cast<const i64 *>(noise), bsk, (int)P->lwe_dim,
                              (int)P->glwe_dim, (int)P->poly_size, (int)P->pbs_base_log, (int)P->pbs_level,
                              sz_stream(stream));

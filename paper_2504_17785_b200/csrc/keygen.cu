@@ -86,6 +86,25 @@ __global__ void bsk_generate_kernel(const u64 *lwe_key, const u64 *glwe_key, con
   if (threadIdx.x == 0) G[(size_t)r * N] += lwe_key[i] << (64 - j * base_log);
 }
 
+// BSK rows for large N: copy masks into G, then (after the GLWE body kernel)
+// add s_i * q / B^j to component r.
+__global__ void bsk_rows_copy_kernel(const u64 *mask, u64 *bsk, long rows_total, int N) {
+  const long total = rows_total * (long)N;
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long ir = e / N;
+    const int c = (int)(e % N);
+    bsk[(size_t)ir * 2 * N + c] = mask[(size_t)ir * N + c];
+  }
+}
+__global__ void bsk_rows_finish_kernel(const u64 *lwe_key, u64 *bsk, long rows_total, int level, int N, int base_log) {
+  const long ir = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (ir >= rows_total) return;
+  const int rows = 2 * level;
+  const int i = (int)(ir / rows), row = (int)(ir % rows);
+  const int r = row / level, j = row % level + 1;
+  bsk[((size_t)ir * 2 + r) * N] += lwe_key[i] << (64 - j * base_log);
+}
+
 // ----------------------------------------------------------------- KSK gen
 // KSK[j][t] = (a, <a, s> + e + s_in[j] * 2^{64 - t beta}); one warp per row (C3).
 __global__ void ksk_generate_kernel(const u64 *in_key, const u64 *lwe_key, const u64 *mask,
@@ -163,6 +182,21 @@ int launch_lwe_encrypt(const u64 *mask, const i64 *noise, const u64 *pt, const u
 int launch_lwe_phase(const u64 *ct, const u64 *key, int dim, size_t count, u64 *phase, cudaStream_t st) {
   const long blocks = (long)((count + 7) / 8);
   lwe_phase_kernel<<<(unsigned)blocks, 256, 0, st>>>(ct, key, dim, (long)count, phase);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+int launch_glwe_body_huge(const u64 *, size_t, const u64 *, const i64 *, u64 *, size_t, long, void *, cudaStream_t);
+
+int launch_bsk_generate_huge(const u64 *lwe_key, const u64 *glwe_key, const u64 *mask, const i64 *noise, u64 *bsk,
+                             int n, int N, int base_log, int level, void *workspace, cudaStream_t st) {
+  const long rows_total = (long)n * 2 * level;
+  bsk_rows_copy_kernel<<<148 * 8, 256, 0, st>>>(mask, bsk, rows_total, N);
+  SZ_LAUNCH_OK();
+  int rc = launch_glwe_body_huge(mask, (size_t)N, glwe_key, noise, bsk + N, (size_t)2 * N, rows_total, workspace, st);
+  if (rc) return rc;
+  bsk_rows_finish_kernel<<<(unsigned)((rows_total + 255) / 256), 256, 0, st>>>(lwe_key, bsk, rows_total, level, N,
+                                                                              base_log);
   SZ_LAUNCH_OK();
   return SILENZIO_OK;
 }

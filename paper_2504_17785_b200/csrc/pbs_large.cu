@@ -13,6 +13,7 @@
 // synchronisation and no workspace.
 #include <cmath>
 #include <mutex>
+#include <vector>
 
 #include "fft.cuh"
 
@@ -368,6 +369,429 @@ int launch_bsk_to_fourier_large(const u64 *bsk, void *fbsk, const silenzio_param
   SZ_CUDA_OK(cudaFuncSetAttribute(bsk_to_fourier_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long blocks = (long)P->lwe_dim * A.rows * 2 * A.P;
   bsk_to_fourier_large_kernel<<<(unsigned)blocks, kTL, smem, stream>>>(A);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+
+// =====================================================================
+// N = 32768 (parameter set B, BASELINE configs[4] 8-bit stage).
+// M = 16384 = 4 x 4096. Negacyclic transform of one polynomial:
+//   Z[q + 4k'] = DFT_4096(y_q)[k'],  y_q[p] = W_M^{pq} sum_{m'<4} z[p + 4096 m'] W_4^{m' q},
+//   z_j = (a_j + i a_{j+M}) w^j, w = e^{i pi / 32768}.
+// fwd_fft_L computes DFT_4096(x_p w8^p) (w8 = e^{i pi / 8192}, the N=8192
+// twist), so the input handed to it is
+//   x_q[p] = F[q][p] sum_{m'} (a_{p+4096m'} + i a_{p+4096m'+M}) C[m'][q],
+//   F[q][p] = e^{i pi p (4q - 3) / 32768},  C[m'][q] = e^{i pi m'/8} i^{m' q}.
+// The inverse applies inv_fft_L per block then the conjugate combination.
+// Per ciphertext the state lives in global memory (L2-resident by limiting
+// the ciphertexts in flight): ACC [2][32768] u64, spectra [rows][4][4096]
+// complex, block scratch [4][4096] complex. One 256-thread CTA per ciphertext.
+constexpr int kNH = 32768;
+constexpr int kMH = 16384;
+constexpr int kLog2_2NH = 16;
+constexpr int kHInFlight = 48;
+
+__device__ double2 g_FH[4 * 4096];  // F[q][p]
+__constant__ double2 c_CH[16];     // C[m'][q], index m' * 4 + q
+
+static std::once_flag g_tabH_once[64];
+static int g_tabH_status[64];
+
+static int init_tabH(int dev) {
+  std::vector<double2> F(4 * 4096);
+  const long double PI = 3.141592653589793238462643383279502884L;
+  for (int q = 0; q < 4; q++)
+    for (int p = 0; p < 4096; p++) {
+      long double ang = PI * (long double)p * (long double)(4 * q - 3) / 32768.0L;
+      F[q * 4096 + p] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+  double2 C[16];
+  for (int mp = 0; mp < 4; mp++)
+    for (int q = 0; q < 4; q++) {
+      long double ang = PI * (long double)mp / 8.0L + PI / 2.0L * (long double)((mp * q) % 4);
+      C[mp * 4 + q] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  if (prev != dev && cudaSetDevice(dev) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  cudaError_t e = cudaMemcpyToSymbol(g_FH, F.data(), F.size() * sizeof(double2));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_CH, C, sizeof(C));
+  if (prev != dev) cudaSetDevice(prev);
+  return e == cudaSuccess ? SILENZIO_OK : SILENZIO_ERR_CUDA;
+}
+
+static int ensure_tables_huge() {
+  int st = ensure_tables_large();
+  if (st) return st;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SILENZIO_ERR_CUDA;
+  std::call_once(g_tabH_once[dev], [dev] { g_tabH_status[dev] = init_tabH(dev); });
+  return g_tabH_status[dev];
+}
+
+__host__ __device__ constexpr size_t brh_ws_per_ct(int rows) {
+  return 2 * (size_t)kNH * sizeof(u64) + (size_t)rows * kMH * sizeof(double2) + (size_t)kMH * sizeof(double2);
+}
+
+struct BRHArgs {
+  const u64 *lwe_small;
+  const u32 *lut_ids;
+  const u64 *luts;
+  u32 num_luts;
+  const double2 *fbsk;  // [n][2][rows][P][4 blocks][16][256]
+  u64 *lwe_out;
+  long count;
+  int n, base_log, w;
+  unsigned char *ws;    // gridDim.x * brh_ws_per_ct(rows)
+};
+
+// forward radix-4 step of one polynomial given by a coefficient functor:
+// writes x_q[p] (input of block q's fwd_fft_L, natural order p = t + 256 m) to X[q][m][t]
+template <class Coef>
+__device__ __forceinline__ void huge_radix4_in(double2 *X, int t, Coef coef) {
+#pragma unroll 1
+  for (int m = 0; m < 16; m++) {
+    const int p = t + 256 * m;
+    double2 v[4];
+#pragma unroll
+    for (int mp = 0; mp < 4; mp++) {
+      const int j = p + 4096 * mp;
+      v[mp] = make_double2(coef(j), coef(j + kMH));
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int mp = 0; mp < 4; mp++) s = cadd(s, cmul(v[mp], c_CH[mp * 4 + q]));
+      X[((size_t)q * 16 + m) * 256 + t] = cmul(s, g_FH[q * 4096 + p]);
+    }
+  }
+}
+
+template <int L, int P>
+__global__ void __launch_bounds__(256, 1) blind_rotate_huge_kernel(BRHArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int rows = 2 * L;
+  double2 *buf = reinterpret_cast<double2 *>(smem);  // [4096] exchange
+  unsigned short *abar = reinterpret_cast<unsigned short *>(buf + kML);
+  const int t = threadIdx.x;
+  const int n = A.n, w = A.w, blog = A.base_log;
+  unsigned char *ws = A.ws + (size_t)blockIdx.x * brh_ws_per_ct(rows);
+  u64 *acc = reinterpret_cast<u64 *>(ws);                                     // [2][32768]
+  double2 *spec = reinterpret_cast<double2 *>(ws + 2 * (size_t)kNH * 8);      // [rows][4][16][256]
+  double2 *X = spec + (size_t)rows * kMH;                                     // [4][16][256]
+
+  for (long c = blockIdx.x; c < A.count; c += gridDim.x) {
+    const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
+    for (int i = t; i < n; i += 256) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2NH);
+    const int bt = (int)sz_modswitch(lwe[n], kLog2_2NH);
+    u32 id = A.lut_ids ? A.lut_ids[c] : 0u;
+    if (id >= A.num_luts) id = 0;
+    const u64 *v = A.luts + (size_t)id * kNH;
+    for (int j = t; j < kNH; j += 256) {
+      acc[j] = 0;
+      const int idx = (j + bt) & (2 * kNH - 1);
+      acc[kNH + j] = (idx < kNH) ? v[idx] : (u64)0 - v[idx - kNH];
+    }
+    __syncthreads();
+    for (int i = 0; i < n; i++) {
+      const int a = abar[i];
+      // -------- forward: every (r, lvl) digit polynomial -> 4 block spectra
+#pragma unroll 1
+      for (int r = 0; r < 2; r++) {
+        const u64 *accr = acc + (size_t)r * kNH;
+#pragma unroll 1
+        for (int lvl = 1; lvl <= L; lvl++) {
+          huge_radix4_in(X, t, [&](int j) {
+            const int src = (j - a) & (2 * kNH - 1);
+            const u64 rv = accr[src & (kNH - 1)];
+            const u64 rot = (src < kNH) ? rv : (u64)0 - rv;
+            u64 rr = sz_decomp_round(rot - accr[j], blog, L);
+            i64 d = 0;
+#pragma unroll
+            for (int tt = L; tt >= 1; tt--) {
+              const i64 dd = sz_decomp_next(rr, blog);
+              if (tt == lvl) d = dd;
+            }
+            return (double)d;
+          });
+          const int row = r * L + (lvl - 1);
+#pragma unroll 1
+          for (int q = 0; q < 4; q++) {
+            double2 x[16];
+#pragma unroll
+            for (int m = 0; m < 16; m++) x[m] = X[((size_t)q * 16 + m) * 256 + t];
+            fwd_fft_L(x, buf, t);
+            double2 *dst = spec + ((size_t)row * 4 + q) * kML;
+#pragma unroll
+            for (int sl = 0; sl < 16; sl++) dst[sl * 256 + t] = x[sl];
+          }
+        }
+      }
+      __syncthreads();  // ACC reads done before the inverse updates it
+      // -------- inverse: per output o and limb p
+#pragma unroll 1
+      for (int o = 0; o < 2; o++) {
+        u64 *acco = acc + (size_t)o * kNH;
+#pragma unroll 1
+        for (int p = P - 1; p >= 0; p--) {
+#pragma unroll 1
+          for (int q = 0; q < 4; q++) {
+            double2 y[16];
+#pragma unroll
+            for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
+#pragma unroll 1
+            for (int row = 0; row < rows; row++) {
+              const double2 *G = A.fbsk + (((((size_t)i * 2 + o) * rows + row) * P + p) * 4 + q) * kML + t;
+              const double2 *D = spec + ((size_t)row * 4 + q) * kML + t;
+#pragma unroll
+              for (int sl = 0; sl < 16; sl++) cmac(y[sl], D[sl * 256], __ldg(&G[sl * 256]));
+            }
+            inv_fft_L(y, buf, t);
+#pragma unroll
+            for (int m = 0; m < 16; m++) X[((size_t)q * 16 + m) * 256 + t] = y[m];
+          }
+          // conjugate radix-4 combination, untwist folded in conj(F), conj(C); round; ACC +=
+#pragma unroll 1
+          for (int m = 0; m < 16; m++) {
+            const int pp = t + 256 * m;
+            double2 u[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++) u[q] = cmulc(X[((size_t)q * 16 + m) * 256 + t], g_FH[q * 4096 + pp]);
+#pragma unroll
+            for (int mp = 0; mp < 4; mp++) {
+              double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int q = 0; q < 4; q++) s = cadd(s, cmulc(u[q], c_CH[mp * 4 + q]));
+              const int j = pp + 4096 * mp;
+              acco[j] += limb_to_torus_L(s.x, p, P, w);
+              acco[j + kMH] += limb_to_torus_L(s.y, p, P, w);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    u64 *out = A.lwe_out + (size_t)c * (kNH + 1);
+    for (int j = t; j <= kNH; j += 256) {
+      u64 val;
+      if (j == 0) val = acc[0];
+      else if (j < kNH) val = (u64)0 - acc[kNH - j];
+      else val = acc[kNH];
+      out[j] = val;
+    }
+    __syncthreads();
+  }
+}
+
+// BSK -> Fourier at N = 32768: one CTA per (i, row, o, limb); the radix-4 inputs
+// of each block are recomputed in registers (offline conversion, no scratch).
+struct B2FHArgs {
+  const u64 *bsk;  // [n][rows][2][N]
+  double2 *fbsk;   // [n][2][rows][P][4][16][256]
+  int rows, P, w;
+  long total;
+};
+
+__global__ void __launch_bounds__(256) bsk_to_fourier_huge_kernel(B2FHArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double2 *buf = reinterpret_cast<double2 *>(smem);
+  const int t = threadIdx.x;
+  for (long blk0 = blockIdx.x; blk0 < A.total; blk0 += gridDim.x) {
+    long blk = blk0;
+    const int p = blk % A.P; blk /= A.P;
+    const int o = blk % 2; blk /= 2;
+    const int row = blk % A.rows; blk /= A.rows;
+    const long i = blk;
+    const u64 *g = A.bsk + (((size_t)i * A.rows + row) * 2 + o) * kNH;
+    double2 *dst = A.fbsk + ((((size_t)i * 2 + o) * A.rows + row) * A.P + p) * (size_t)kMH;
+    const double scale = 1.0 / kMH;
+#pragma unroll 1
+    for (int q = 0; q < 4; q++) {
+      double2 x[16];
+#pragma unroll 1
+      for (int m = 0; m < 16; m++) {
+        const int pp = t + 256 * m;
+        double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int mp = 0; mp < 4; mp++) {
+          const int j = pp + 4096 * mp;
+          const double2 v = make_double2(limb_of(g[j], A.P, A.w, p), limb_of(g[j + kMH], A.P, A.w, p));
+          s = cadd(s, cmul(v, c_CH[mp * 4 + q]));
+        }
+        x[m] = cmul(s, g_FH[q * 4096 + pp]);
+      }
+      fwd_fft_L(x, buf, t);
+#pragma unroll
+      for (int sl = 0; sl < 16; sl++)
+        dst[(size_t)q * kML + sl * 256 + t] = make_double2(x[sl].x * scale, x[sl].y * scale);
+      __syncthreads();
+    }
+  }
+}
+
+size_t blind_rotate_huge_ws_bytes(const silenzio_params *P, size_t count) {
+  const long inflight = (long)count < kHInFlight ? (long)count : kHInFlight;
+  return (size_t)inflight * brh_ws_per_ct(2 * (int)P->pbs_level);
+}
+
+long blind_rotate_huge_wave(const silenzio_params *P) {
+  (void)P;
+  return kHInFlight;
+}
+
+int launch_blind_rotate_huge(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
+                             const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
+                             void *workspace, cudaStream_t stream) {
+  int st = ensure_tables_huge();
+  if (st) return st;
+  if (!workspace) return SILENZIO_ERR_WORKSPACE;
+  BRHArgs A;
+  A.lwe_small = lwe_small;
+  A.lut_ids = lut_ids;
+  A.luts = luts;
+  A.num_luts = num_luts;
+  A.fbsk = reinterpret_cast<const double2 *>(fbsk);
+  A.lwe_out = lwe_out;
+  A.n = (int)P->lwe_dim;
+  A.base_log = (int)P->pbs_base_log;
+  A.w = (int)P->limb_bits;
+  A.ws = reinterpret_cast<unsigned char *>(workspace);
+  void (*kern)(BRHArgs) = nullptr;
+  const int L = (int)P->pbs_level, PP = (int)P->fft_limbs;
+  if (L == 2 && PP == 3) kern = blind_rotate_huge_kernel<2, 3>;
+  if (L == 4 && PP == 3) kern = blind_rotate_huge_kernel<4, 3>;
+  if (L == 1 && PP == 3) kern = blind_rotate_huge_kernel<1, 3>;
+  if (!kern) return SILENZIO_ERR_UNSUPPORTED;
+  const size_t smem = kML * sizeof(double2) + ((size_t)A.n * 2 + 15) / 16 * 16;
+  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (long c0 = 0; c0 < (long)count; c0 += kHInFlight) {
+    BRHArgs W = A;
+    const long cnt = ((long)count - c0 < kHInFlight) ? (long)count - c0 : kHInFlight;
+    W.lwe_small = A.lwe_small + (size_t)c0 * (A.n + 1);
+    W.lut_ids = A.lut_ids ? A.lut_ids + c0 : nullptr;
+    W.lwe_out = A.lwe_out + (size_t)c0 * (kNH + 1);
+    W.count = cnt;
+    kern<<<(unsigned)cnt, 256, smem, stream>>>(W);
+    SZ_LAUNCH_OK();
+  }
+  return SILENZIO_OK;
+}
+
+int launch_bsk_to_fourier_huge(const u64 *bsk, void *fbsk, const silenzio_params *P, cudaStream_t stream) {
+  int st = ensure_tables_huge();
+  if (st) return st;
+  B2FHArgs A;
+  A.bsk = bsk;
+  A.fbsk = reinterpret_cast<double2 *>(fbsk);
+  A.rows = 2 * (int)P->pbs_level;
+  A.P = (int)P->fft_limbs;
+  A.w = (int)P->limb_bits;
+  A.total = (long)P->lwe_dim * A.rows * 2 * A.P;
+  const int grid = 296;
+  const size_t smem = kML * sizeof(double2);
+  SZ_CUDA_OK(cudaFuncSetAttribute(bsk_to_fourier_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  bsk_to_fourier_huge_kernel<<<grid, 256, smem, stream>>>(A);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+}  // namespace sz
+
+namespace sz {
+
+// GLWE bodies at N = 32768 for key generation: body = E + A * S (negacyclic,
+// binary S), exact via three 22/22/20-bit limbs of A and the f64 transform
+// above (|sum| <= 2^21 * 16384 < 2^53, rounded to the exact integer).
+// One CTA per GLWE (grid-stride); scratch per CTA: X, S^ (2 x 256 KiB) + res (256 KiB).
+struct GBHArgs {
+  const u64 *A;      // row g: A + g * a_stride
+  const u64 *key;    // [N] binary
+  const i64 *E;      // row g: E + g * N
+  u64 *body;         // row g: body + g * out_stride
+  long count;
+  size_t a_stride, out_stride;
+  unsigned char *ws;
+};
+
+__host__ __device__ constexpr size_t gbh_ws_per_cta() { return 2 * (size_t)kMH * sizeof(double2) + (size_t)kNH * sizeof(u64); }
+
+__global__ void __launch_bounds__(256) glwe_body_huge_kernel(GBHArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double2 *buf = reinterpret_cast<double2 *>(smem);
+  const int t = threadIdx.x;
+  unsigned char *ws = A.ws + (size_t)blockIdx.x * gbh_ws_per_cta();
+  double2 *X = reinterpret_cast<double2 *>(ws);
+  double2 *Sh = X + kMH;
+  u64 *res = reinterpret_cast<u64 *>(Sh + kMH);
+  // S^ once per CTA
+  huge_radix4_in(X, t, [&](int j) { return (double)(A.key[j] & 1); });
+#pragma unroll 1
+  for (int q = 0; q < 4; q++) {
+    double2 x[16];
+#pragma unroll
+    for (int m = 0; m < 16; m++) x[m] = X[((size_t)q * 16 + m) * 256 + t];
+    fwd_fft_L(x, buf, t);
+#pragma unroll
+    for (int sl = 0; sl < 16; sl++) Sh[(size_t)q * kML + sl * 256 + t] = make_double2(x[sl].x / kMH, x[sl].y / kMH);
+    __syncthreads();
+  }
+  for (long g = blockIdx.x; g < A.count; g += gridDim.x) {
+    const u64 *a = A.A + (size_t)g * A.a_stride;
+    const i64 *e = A.E + (size_t)g * kNH;
+    for (int j = t; j < kNH; j += 256) res[j] = (u64)e[j];
+#pragma unroll 1
+    for (int p = 0; p < 3; p++) {
+      __syncthreads();
+      huge_radix4_in(X, t, [&](int j) { return limb_of(a[j], 3, 22, p); });
+#pragma unroll 1
+      for (int q = 0; q < 4; q++) {
+        double2 x[16];
+#pragma unroll
+        for (int m = 0; m < 16; m++) x[m] = X[((size_t)q * 16 + m) * 256 + t];
+        fwd_fft_L(x, buf, t);
+#pragma unroll
+        for (int sl = 0; sl < 16; sl++) x[sl] = cmul(x[sl], Sh[(size_t)q * kML + sl * 256 + t]);
+        inv_fft_L(x, buf, t);
+#pragma unroll
+        for (int m = 0; m < 16; m++) X[((size_t)q * 16 + m) * 256 + t] = x[m];
+      }
+#pragma unroll 1
+      for (int m = 0; m < 16; m++) {
+        const int pp = t + 256 * m;
+        double2 u[4];
+#pragma unroll
+        for (int q = 0; q < 4; q++) u[q] = cmulc(X[((size_t)q * 16 + m) * 256 + t], g_FH[q * 4096 + pp]);
+#pragma unroll
+        for (int mp = 0; mp < 4; mp++) {
+          double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+          for (int q = 0; q < 4; q++) s = cadd(s, cmulc(u[q], c_CH[mp * 4 + q]));
+          const int j = pp + 4096 * mp;
+          res[j] += (u64)__double2ll_rn(s.x) << (22 * p);
+          res[j + kMH] += (u64)__double2ll_rn(s.y) << (22 * p);
+        }
+      }
+    }
+    __syncthreads();
+    u64 *out = A.body + (size_t)g * A.out_stride;
+    for (int j = t; j < kNH; j += 256) out[j] = res[j];
+  }
+}
+
+size_t glwe_body_huge_ws_bytes() { return 148 * gbh_ws_per_cta(); }
+
+int launch_glwe_body_huge(const u64 *Amask, size_t a_stride, const u64 *key, const i64 *E, u64 *body,
+                          size_t out_stride, long count, void *workspace, cudaStream_t stream) {
+  int st = ensure_tables_huge();
+  if (st) return st;
+  if (!workspace) return SILENZIO_ERR_WORKSPACE;
+  GBHArgs A{Amask, key, E, body, count, a_stride, out_stride, reinterpret_cast<unsigned char *>(workspace)};
+  const size_t smem = kML * sizeof(double2);
+  SZ_CUDA_OK(cudaFuncSetAttribute(glwe_body_huge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const long grid = count < 148 ? count : 148;
+  glwe_body_huge_kernel<<<(unsigned)grid, 256, smem, stream>>>(A);
   SZ_LAUNCH_OK();
   return SILENZIO_OK;
 }

@@ -47,13 +47,15 @@ def load():
         "silenzio_bsk_to_fourier": ([V, V, P, V], I),
         "silenzio_keyswitch_batch": ([V, V, V, S, P, V], I),
         "silenzio_pbs_batch": ([V, V, V, U32, V, V, V, S, P, V, V], I),
-        "silenzio_blind_rotate_batch": ([V, V, V, U32, V, V, S, P, V], I),
+        "silenzio_blind_rotate_batch": ([V, V, V, U32, V, V, S, P, V, V], I),
+        "silenzio_blind_rotate_workspace_bytes": ([P, S], S),
         "silenzio_pbs_batch_host": ([V, V, V, U32, V, V, V, S, S, P, V], I),
         "silenzio_lwe_linear_batch": ([V, V, V, V, U32, U32, S, V, V], I),
         "silenzio_build_testpoly": ([V, U32, U32, U32, V, V], I),
         "silenzio_lwe_encrypt_batch": ([V, V, V, V, U32, S, V, V], I),
         "silenzio_lwe_phase_batch": ([V, V, U32, S, V, V], I),
-        "silenzio_bsk_generate": ([V, V, V, V, V, P, V], I),
+        "silenzio_bsk_generate": ([V, V, V, V, V, P, V, V], I),
+        "silenzio_bsk_generate_workspace_bytes": ([P], S),
         "silenzio_ksk_generate": ([V, V, V, V, V, U32, U32, U32, U32, V], I),
         "silenzio_rns_matmul_workspace_bytes": ([P, U32, U32, U32], S),
         "silenzio_rns_matmul": ([V, V, U32, U32, U32, V, U32, V, V, V, P, V, S, V], I),
@@ -76,9 +78,9 @@ def exported_symbols():
         "silenzio_status_string", "silenzio_version", "silenzio_fourier_bsk_bytes",
         "silenzio_pbs_workspace_bytes", "silenzio_pbs_host_workspace_bytes", "silenzio_pbs_launch_count",
         "silenzio_bsk_to_fourier", "silenzio_keyswitch_batch", "silenzio_pbs_batch",
-        "silenzio_blind_rotate_batch", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
+        "silenzio_blind_rotate_batch", "silenzio_blind_rotate_workspace_bytes", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
         "silenzio_build_testpoly", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
-        "silenzio_bsk_generate", "silenzio_ksk_generate", "silenzio_rns_matmul_workspace_bytes",
+        "silenzio_bsk_generate", "silenzio_bsk_generate_workspace_bytes", "silenzio_ksk_generate", "silenzio_rns_matmul_workspace_bytes",
         "silenzio_rns_matmul", "silenzio_gadget_workspace_bytes", "silenzio_rns2mrns",
         "silenzio_rns_sign_abs", "silenzio_mrns_bitlen_max", "silenzio_int_ce_grad",
     ]
@@ -181,14 +183,21 @@ def pbs_batch(lwe_in, lut_ids, luts, fourier_bsk, ksk, P, out=None, workspace=No
     return out
 
 
-def blind_rotate_batch(lwe_small, lut_ids, luts, fourier_bsk, P, out=None, stream=None):
+def blind_rotate_workspace_bytes(P, count: int) -> int:
+    return load().silenzio_blind_rotate_workspace_bytes(ctypes.byref(make_params(P)), count)
+
+
+def blind_rotate_batch(lwe_small, lut_ids, luts, fourier_bsk, P, out=None, workspace=None, stream=None):
     count = lwe_small.shape[0]
     if out is None:
         out = torch.empty((count, P.k * P.N + 1), dtype=torch.int64, device=lwe_small.device)
+    if workspace is None:
+        nb = blind_rotate_workspace_bytes(P, count)
+        workspace = torch.empty(nb, dtype=torch.uint8, device=lwe_small.device) if nb else None
     num_luts = luts.shape[0] if luts.dim() == 2 else 1
     _check(load().silenzio_blind_rotate_batch(_ptr(lwe_small), _ptr(lut_ids), _ptr(luts), num_luts,
                                               _ptr(fourier_bsk), _ptr(out), count,
-                                              ctypes.byref(make_params(P)), _stream(stream)))
+                                              ctypes.byref(make_params(P)), _ptr(workspace), _stream(stream)))
     return out
 
 
@@ -239,8 +248,10 @@ def lwe_phase_batch(ct, key, out=None, stream=None):
 def bsk_generate(lwe_key, glwe_key, mask, noise, P, stream=None):
     rows = (P.k + 1) * P.pbs_level
     out = torch.empty((P.n, rows, P.k + 1, P.N), dtype=torch.int64, device=mask.device)
+    nb = load().silenzio_bsk_generate_workspace_bytes(ctypes.byref(make_params(P)))
+    ws = torch.empty(nb, dtype=torch.uint8, device=mask.device) if nb else None
     _check(load().silenzio_bsk_generate(_ptr(lwe_key), _ptr(glwe_key), _ptr(mask), _ptr(noise), _ptr(out),
-                                        ctypes.byref(make_params(P)), _stream(stream)))
+                                        ctypes.byref(make_params(P)), _ptr(ws), _stream(stream)))
     return out
 
 

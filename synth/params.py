@@ -85,6 +85,14 @@ PARAMS = {
                         pbs_level=4, ks_base_log=8, ks_level=8,
                         lwe_sigma_log2=NOISELESS, glwe_sigma_log2=NOISELESS,
                         p=6),
+    # Set-B-shaped (N=32768, 2^15 x 2, 8-bit) with a small n for oracle replays.
+    "B_SMALLN": Params("B_SMALLN", n=6, k=1, N=32768, pbs_base_log=15, pbs_level=2,
+                       ks_base_log=4, ks_level=5, lwe_sigma_log2=-23.0,
+                       glwe_sigma_log2=-51.0, p=8),
+    "EXACT32768": Params("EXACT32768", n=3, k=1, N=32768, pbs_base_log=16,
+                         pbs_level=4, ks_base_log=8, ks_level=8,
+                         lwe_sigma_log2=NOISELESS, glwe_sigma_log2=NOISELESS,
+                         p=8),
     "EXACT2048": Params("EXACT2048", n=8, k=1, N=2048, pbs_base_log=16,
                         pbs_level=4, ks_base_log=8, ks_level=8,
                         lwe_sigma_log2=NOISELESS, glwe_sigma_log2=NOISELESS,

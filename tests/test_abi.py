@@ -54,9 +54,9 @@ def test_host_side_sizing_and_validation(lib):
     bad.fft_limbs = 4
     assert silenzio.load().silenzio_fourier_bsk_bytes(ctypes.byref(bad)) == 0
     L = silenzio.load()
-    # unsupported shape (N = 32768 blind rotation not in this build) is reported, not run
-    B = get_params("B")
-    rc = L.silenzio_bsk_to_fourier(ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.byref(silenzio.make_params(B)), None)
+    # unsupported shape (GLWE dimension k = 2 has no kernel) is reported, not run
+    K2 = get_params("A", k=2)
+    rc = L.silenzio_bsk_to_fourier(ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.byref(silenzio.make_params(K2)), None)
     assert rc == -2
     # null pointers are rejected before any launch
     rc = L.silenzio_pbs_batch(None, None, None, 1, None, None, None, 5, ctypes.byref(silenzio.make_params(P)), None, None)
