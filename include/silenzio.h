@@ -200,6 +200,24 @@ int silenzio_int_ce_grad(const uint64_t *Yhat, const uint64_t *Y, uint32_t a, ui
                          const void *fourier_bsk, const uint64_t *ksk, const silenzio_params *params,
                          void *workspace, size_t workspace_bytes, void *stream);
 
+/* g7: Shift2MSBs+- digit combine with the 8-bit stage (Alg. 3 steps 3-6, Alg. 4
+ * re-sign; DESIGN.md §Config 4). Inputs at set A (pa): top_digit [count] = most
+ * significant MRNS digit of x (sign: >= top_radix / 2), abs_digits [k][count] =
+ * MRNS digits of |x|, maxes [k] = silenzio_mrns_bitlen_max output. One 8-bit PBS
+ * at set B (pb, N = 32768) per element and digit, reached through keyswitches
+ * ksk_ab (pab: set-A big key -> set-B small key) and ksk_ba (pba: set-B big key
+ * -> set-A big key). Output out [count] = Shift2MSBs+-(x) in [-(2^gamma - 1),
+ * 2^gamma - 1] at Delta (set A); maxbit_out [1] = encrypted maxBit at 2^55
+ * (shift = maxBit - gamma). */
+size_t silenzio_mrns_combine_workspace_bytes(const silenzio_params *pa, const silenzio_params *pb, uint32_t k,
+                                             size_t count);
+int silenzio_mrns_digit_combine(const uint64_t *top_digit, const uint64_t *abs_digits, const uint64_t *maxes,
+                                uint32_t k, size_t count, uint32_t top_radix, uint32_t w, uint32_t gamma,
+                                uint64_t *out, uint64_t *maxbit_out, const void *fbsk_a, const uint64_t *ksk_a,
+                                const silenzio_params *pa, const void *fbsk_b, const silenzio_params *pb,
+                                const uint64_t *ksk_ab, const silenzio_params *pab, const uint64_t *ksk_ba,
+                                const silenzio_params *pba, void *workspace, size_t workspace_bytes, void *stream);
+
 /* ------------------------------------- client-side key / ciphertext generation
  * All random numbers are inputs (drawn by the caller), so every key and
  * ciphertext is a deterministic function of the caller's seeded draws. */

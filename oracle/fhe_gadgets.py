@@ -262,3 +262,80 @@ def int_ce_grad_fhe(ctx: Ctx, Yhat, Y):
     Z = axpy([(1, Ep), (-1, A2), (-1, B2)])
     out = ctx.lut(Z, [table(-13, lambda v: (v > 0) - (v < 0), DELTA_LOG)])
     return out.reshape(a, b, -1)
+
+
+# ------------------------------------------------------- g7: 8-bit combine
+DELTA_B_LOG = 55  # set B: p = 8 + padding
+
+
+def table_b(window_start: int, f_raw) -> np.ndarray:
+    """256 torus values realising f on [w0, w0+256) of Z_512 (set B, p = 8)."""
+    tab = [0] * 256
+    for x in range(window_start, window_start + 256):
+        xm = x % 512
+        v = _u(f_raw(x))
+        if xm < 256:
+            tab[xm] = v
+        else:
+            tab[xm - 256] = _u(-v)
+    return np.array(tab, dtype=np.uint64)
+
+
+class CtxB:
+    """8-bit PBS from set-A big-key ciphertexts back to set-A big-key ciphertexts:
+    KS (A big -> B small) -> BR at set B -> SE (B big) -> KS (B big -> A big)."""
+
+    def __init__(self, PB, KB, ksk_ab, ks_ab, ksk_ba, ks_ba):
+        self.PB, self.KB = PB, KB
+        self.ksk_ab, self.ks_ab = ksk_ab, ks_ab      # (in_dim, n_out, base_log, level)
+        self.ksk_ba, self.ks_ba = ksk_ba, ks_ba
+        self.pbs_count = 0
+
+    def lut(self, cts, tables, ids=None):
+        cts = np.ascontiguousarray(np.asarray(cts, dtype=np.uint64).reshape(-1, cts.shape[-1]))
+        small = T.keyswitch_dims(cts, self.ksk_ab, *self.ks_ab)
+        polys = np.stack([T.test_polynomial(t, 8, self.PB.N) for t in tables])
+        ids = np.zeros(len(cts), np.uint32) if ids is None else np.asarray(ids, np.uint32)
+        big = T.br_se(small, ids, polys, self.KB["bsk"], self.PB)
+        self.pbs_count += len(cts)
+        return T.keyswitch_dims(big, self.ksk_ba, *self.ks_ba)
+
+
+def digit_combine_fhe(ctx: Ctx, cb: CtxB, top_digit, abs_digits, maxes, top_radix, w, gamma):
+    """Alg. 3 steps 3-6 + Alg. 4 re-sign with the 8-bit stage (DESIGN.md §Config 4)."""
+    k = len(abs_digits)
+    eB = ctx.lut(top_digit, [table_raw(0, lambda y: (1 << 62) if 2 * y >= top_radix else 0)])
+    dB = np.stack([ctx.lut(d, [table(0, lambda v: v, DELTA_B_LOG)]) for d in abs_digits])
+    v = np.stack([ctx.lut(maxes[i:i + 1], [table(0, lambda M, i=i: M + w * i if M > 0 else 0, DELTA_B_LOG)])[0]
+                  for i in range(k)])
+    relu = table_b(-128, lambda t: max(t, 0) << DELTA_B_LOG)
+    mb = v[0].copy()
+    for i in range(1, k):
+        t = axpy([(1, mb), (-1, v[i])])
+        r = cb.lut(t[None], [relu])[0]
+        mb = axpy([(1, v[i]), (1, r)])
+
+    def shift_table(i):
+        def f(x):
+            ds = (gamma + w * i - x) if x > w else 0
+            ds = max(-4, min(gamma - 1, ds))
+            return ((ds + 4) * 16) << DELTA_B_LOG
+        return table_b(0, f)
+
+    S = cb.lut(np.stack([mb] * k), [shift_table(i) for i in range(k)], list(range(k)))
+
+    def comb(x):
+        neg, s, d = x >> 7, ((x >> 4) & 7) - 4, x & 15
+        lsh = min(max(s, 0), gamma - 1)
+        rsh = -s if s < 0 else 0
+        val = (d << lsh) >> rsh
+        return (-val if neg else val) << DELTA_LOG
+    tc = table_b(0, comb)
+    R = []
+    for i in range(k):
+        packed = axpy([(1, eB), (1, dB[i]), (1, np.broadcast_to(S[i], dB[i].shape))])
+        R.append(cb.lut(packed, [tc]))
+    out = R[0].copy()
+    for i in range(1, k):
+        out = axpy([(1, out), (1, R[i])])
+    return out, mb

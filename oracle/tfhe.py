@@ -213,3 +213,15 @@ def lwe_linear(ct, idx, coef, cst) -> np.ndarray:
 
 def num_threads() -> int:
     return int(native.lib().oracle_num_threads())
+
+
+def ksk_generate(in_key, out_key, rnd: dict, base_log: int, level: int) -> np.ndarray:
+    """KSK from `in_key` to `out_key` (C3): KSK[j][t] = LWE_out(in_key[j] q/B^t).
+    rnd = synth.cross_ksk_randomness(...)."""
+    in_key, out_key = _u64(in_key), _u64(out_key)
+    in_dim, n = len(in_key), len(out_key)
+    ksk = np.zeros((in_dim, level, n + 1), dtype=np.uint64)
+    native.lib().oracle_ksk_generate(native.ptr(in_key), native.ptr(out_key), native.ptr(_u64(rnd["ksk_mask"])),
+                                     native.ptr(_i64(rnd["ksk_noise"])), in_dim, n, base_log, level,
+                                     native.ptr(ksk))
+    return ksk

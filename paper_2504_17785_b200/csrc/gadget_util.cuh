@@ -19,6 +19,8 @@ size_t silenzio_pbs_workspace_bytes(const silenzio_params *, size_t);
 namespace sz {
 int launch_lwe_axpy3(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc, u64 cst,
                      size_t count, int dim, cudaStream_t st);
+int launch_lwe_axpy_bcast(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc, size_t count,
+                          int dim, cudaStream_t st);
 }
 
 namespace szg {

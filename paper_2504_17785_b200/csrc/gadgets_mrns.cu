@@ -264,3 +264,219 @@ int silenzio_int_ce_grad(const uint64_t *Yhat, const uint64_t *Y, uint32_t a, ui
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// g7: Shift2MSBs+- digit combine with the 8-bit stage (parameter set B).
+// Alg. 3 steps 2-6 + Alg. 4 re-sign (l.419): per digit
+// position i, digitShift_i = (gamma - (maxBit - w i)) * anyShift (clamped to
+// [-4, gamma-1], output-equivalent for 4-bit digits); per element and digit one
+// 8-bit PBS evaluates +-((d << lshift) >> rshift) on the packed index
+// neg * 128 + (S_i + 4) * 16 + d; the digit results are summed.
+// A set-B PBS here = KS (set-A big key -> set-B small key) -> BR at N = 32768
+// -> SE (set-B big key) -> KS (set-B big key -> set-A big key).
+extern "C" {
+int silenzio_keyswitch_batch(const uint64_t *, const uint64_t *, uint64_t *, size_t, const silenzio_params *, void *);
+int silenzio_blind_rotate_batch(const uint64_t *, const uint32_t *, const uint64_t *, uint32_t, const void *,
+                                uint64_t *, size_t, const silenzio_params *, void *, void *);
+size_t silenzio_blind_rotate_workspace_bytes(const silenzio_params *, size_t);
+}
+
+namespace {
+
+constexpr u64 kDeltaB = 1ull << 55;  // set B: p = 8 + padding
+constexpr size_t kBChunk = 2048;
+
+template <class F>
+std::vector<u64> table_window_b(int w0, F f) {  // 256-value window of Z_512
+  std::vector<u64> T(256, 0);
+  for (int x = w0; x < w0 + 256; x++) {
+    const int xm = ((x % 512) + 512) % 512;
+    if (xm < 256) T[xm] = f(x);
+    else T[xm - 256] = (u64)0 - f(x);
+  }
+  return T;
+}
+
+struct DevB {
+  const void *fbsk;
+  const silenzio_params *pb, *pab, *pba;
+  const u64 *ksk_ab, *ksk_ba;
+  u64 *small, *big, *tables, *luts;
+  u32 *ids;
+  void *brws;
+  cudaStream_t st;
+};
+
+size_t devb_bytes(const silenzio_params *pb, uint32_t nluts) {
+  return rup(kBChunk * (pb->lwe_dim + 1) * 8) + rup(kBChunk * ((size_t)pb->glwe_dim * pb->poly_size + 1) * 8) +
+         rup((size_t)nluts * 256 * 8) + rup((size_t)nluts * pb->poly_size * 8) + rup(kBChunk * 4) +
+         rup(silenzio_blind_rotate_workspace_bytes(pb, kBChunk));
+}
+
+int upload_luts_b(DevB &B, const std::vector<std::vector<u64>> &tabs) {
+  std::vector<u64> flat;
+  for (auto &t : tabs) flat.insert(flat.end(), t.begin(), t.end());
+  SZ_CUDA_OK(cudaMemcpyAsync(B.tables, flat.data(), flat.size() * 8, cudaMemcpyHostToDevice, B.st));
+  SZ_CUDA_OK(cudaStreamSynchronize(B.st));
+  return silenzio_build_testpoly(B.tables, (u32)tabs.size(), 8, B.pb->poly_size, B.luts, B.st);
+}
+
+// set-A big-key in -> set-A big-key out through the 8-bit PBS
+int pbs_b(DevB &B, const u64 *in, u64 *out, size_t count, u32 num_luts, const std::vector<u32> &ids) {
+  const size_t ca = (size_t)B.pab->ks_in_dim + 1;  // set-A big LWE words
+  for (size_t c0 = 0; c0 < count; c0 += kBChunk) {
+    const size_t cnt = count - c0 < kBChunk ? count - c0 : kBChunk;
+    const u32 *idp = nullptr;
+    if (!ids.empty()) {
+      SZ_CUDA_OK(cudaMemcpyAsync(B.ids, ids.data() + c0, cnt * 4, cudaMemcpyHostToDevice, B.st));
+      SZ_CUDA_OK(cudaStreamSynchronize(B.st));
+      idp = B.ids;
+    }
+    int rc = silenzio_keyswitch_batch(in + c0 * ca, B.ksk_ab, B.small, cnt, B.pab, B.st);
+    if (rc) return rc;
+    if ((rc = silenzio_blind_rotate_batch(B.small, idp, B.luts, num_luts, B.fbsk, B.big, cnt, B.pb, B.brws, B.st)))
+      return rc;
+    if ((rc = silenzio_keyswitch_batch(B.big, B.ksk_ba, out + c0 * ca, cnt, B.pba, B.st))) return rc;
+  }
+  return SILENZIO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t silenzio_mrns_combine_workspace_bytes(const silenzio_params *pa, const silenzio_params *pb, uint32_t k,
+                                             size_t count) {
+  if (!pa || !pb) return 0;
+  const size_t ct = ct_bytes(pa);
+  return 3 * rup((size_t)k * count * ct) + rup(count * ct) + 4 * rup((size_t)k * ct) +
+         dev_bytes(pa, 4 * count + 64) + devb_bytes(pb, k) + 4096;
+}
+
+int silenzio_mrns_digit_combine(const uint64_t *top_digit, const uint64_t *abs_digits, const uint64_t *maxes,
+                                uint32_t k, size_t count, uint32_t top_radix, uint32_t w, uint32_t gamma,
+                                uint64_t *out, uint64_t *maxbit_out, const void *fbsk_a, const uint64_t *ksk_a,
+                                const silenzio_params *pa, const void *fbsk_b, const silenzio_params *pb,
+                                const uint64_t *ksk_ab, const silenzio_params *pab, const uint64_t *ksk_ba,
+                                const silenzio_params *pba, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!top_digit || !abs_digits || !maxes || !out || !maxbit_out || !fbsk_a || !ksk_a || !pa || !fbsk_b || !pb ||
+      !ksk_ab || !pab || !ksk_ba || !pba)
+    return SILENZIO_ERR_NULL_POINTER;
+  if (!workspace || workspace_bytes < silenzio_mrns_combine_workspace_bytes(pa, pb, k, count))
+    return SILENZIO_ERR_WORKSPACE;
+  if (pa->poly_size != 2048 || pb->poly_size != 32768) return SILENZIO_ERR_UNSUPPORTED;
+  if (pab->ks_in_dim != pa->glwe_dim * pa->poly_size || pab->lwe_dim != pb->lwe_dim ||
+      pba->ks_in_dim != pb->glwe_dim * pb->poly_size || pba->lwe_dim != pa->glwe_dim * pa->poly_size)
+    return SILENZIO_ERR_INVALID_PARAM;
+  if (k == 0 || w * (k - 1) + w > 127 || gamma < 1 || gamma > 4 || top_radix % 2) return SILENZIO_ERR_WINDOW;
+  if (count == 0) return SILENZIO_OK;
+  const size_t cw = ct_bytes(pa) / 8;
+  unsigned char *p = reinterpret_cast<unsigned char *>(workspace);
+  auto carve = [&](size_t bytes) {
+    unsigned char *r = p;
+    p += rup(bytes);
+    return r;
+  };
+  u64 *dB = reinterpret_cast<u64 *>(carve((size_t)k * count * cw * 8));
+  u64 *packed = reinterpret_cast<u64 *>(carve((size_t)k * count * cw * 8));
+  u64 *R = reinterpret_cast<u64 *>(carve((size_t)k * count * cw * 8));
+  u64 *eB = reinterpret_cast<u64 *>(carve(count * cw * 8));
+  u64 *v = reinterpret_cast<u64 *>(carve((size_t)k * cw * 8));
+  u64 *mbk = reinterpret_cast<u64 *>(carve((size_t)k * cw * 8));
+  u64 *S = reinterpret_cast<u64 *>(carve((size_t)k * cw * 8));
+  u64 *tmp = reinterpret_cast<u64 *>(carve((size_t)k * cw * 8));
+  Dev D;
+  dev_init(D, p, pa, fbsk_a, ksk_a, sz_stream(stream), 4 * count + 64);
+  DevB B;
+  B.fbsk = fbsk_b;
+  B.pb = pb;
+  B.pab = pab;
+  B.pba = pba;
+  B.ksk_ab = ksk_ab;
+  B.ksk_ba = ksk_ba;
+  B.st = sz_stream(stream);
+  B.small = reinterpret_cast<u64 *>(carve(kBChunk * (pb->lwe_dim + 1) * 8));
+  B.big = reinterpret_cast<u64 *>(carve(kBChunk * ((size_t)pb->glwe_dim * pb->poly_size + 1) * 8));
+  B.tables = reinterpret_cast<u64 *>(carve((size_t)k * 256 * 8));
+  B.luts = reinterpret_cast<u64 *>(carve((size_t)k * pb->poly_size * 8));
+  B.ids = reinterpret_cast<u32 *>(carve(kBChunk * 4));
+  B.brws = carve(silenzio_blind_rotate_workspace_bytes(pb, kBChunk));
+  int rc;
+  const int rk = (int)top_radix, W = (int)w, g = (int)gamma;
+  // (1) sign bit at 128 Delta_B = 2^62, fresh
+  std::vector<std::vector<u64>> ts = {table_window(0, [rk](int y) { return 2 * y >= rk ? (1ull << 62) : 0ull; })};
+  if ((rc = upload_luts(D, ts))) return rc;
+  if ((rc = lookup(D, top_digit, eB, count, {}, 1))) return rc;
+  // (2) digits rescaled to Delta_B
+  std::vector<std::vector<u64>> td = {table_window(0, [](int d) { return enc(d, kDeltaB); })};
+  if ((rc = upload_luts(D, td))) return rc;
+  if ((rc = lookup(D, abs_digits, dB, (size_t)k * count, {}, 1))) return rc;
+  // (3) v_i = M_i > 0 ? M_i + w i : 0 at Delta_B (one LUT per position)
+  {
+    std::vector<std::vector<u64>> tv;
+    std::vector<u32> ids(k);
+    for (uint32_t i = 0; i < k; i++) {
+      tv.push_back(table_window(0, [i, W](int M) { return enc(M > 0 ? M + W * (int)i : 0, kDeltaB); }));
+      ids[i] = i;
+    }
+    // the Dev holds kMaxLuts (4) test polynomials: evaluate in groups
+    for (uint32_t i0 = 0; i0 < k; i0 += kMaxLuts) {
+      const uint32_t ng = (k - i0 < (uint32_t)kMaxLuts) ? k - i0 : (uint32_t)kMaxLuts;
+      std::vector<std::vector<u64>> grp(tv.begin() + i0, tv.begin() + i0 + ng);
+      std::vector<u32> gids(ids.begin() + i0, ids.begin() + i0 + ng);
+      for (auto &x : gids) x -= i0;
+      if ((rc = upload_luts(D, grp))) return rc;
+      if ((rc = lookup(D, maxes + (size_t)i0 * cw, v + (size_t)i0 * cw, ng, gids, ng))) return rc;
+    }
+  }
+  // (4) maxBit = fold of max(x, y) = y + ReLU_B(x - y) over v_0..v_{k-1} (8-bit window [-128, 128))
+  SZ_CUDA_OK(cudaMemcpyAsync(maxbit_out, v, cw * 8, cudaMemcpyDeviceToDevice, D.st));
+  {
+    std::vector<std::vector<u64>> trelu = {table_window_b(-128, [](int t) { return enc(t > 0 ? t : 0, kDeltaB); })};
+    if ((rc = upload_luts_b(B, trelu))) return rc;
+    for (uint32_t i = 1; i < k; i++) {
+      const u64 *y = v + (size_t)i * cw;
+      if ((rc = axpy3(D, tmp, maxbit_out, 1, y, -1, nullptr, 0, 0, 1))) return rc;        // x - y
+      if ((rc = pbs_b(B, tmp, tmp + cw, 1, 1, {}))) return rc;                             // ReLU
+      if ((rc = axpy3(D, maxbit_out, y, 1, tmp + cw, 1, nullptr, 0, 0, 1))) return rc;    // y + ReLU
+    }
+  }
+  // (5) S'_i = (clamp(digitShift_i, -4, gamma-1) + 4) * 16 * Delta_B
+  {
+    std::vector<std::vector<u64>> tsh;
+    std::vector<u32> ids(k);
+    for (uint32_t i = 0; i < k; i++) {
+      tsh.push_back(table_window_b(0, [i, W, g](int mb) {
+        int ds = (mb > W) ? (g + W * (int)i - mb) : 0;
+        ds = ds < -4 ? -4 : (ds > g - 1 ? g - 1 : ds);
+        return enc((ds + 4) * 16, kDeltaB);
+      }));
+      ids[i] = i;
+      SZ_CUDA_OK(cudaMemcpyAsync(mbk + (size_t)i * cw, maxbit_out, cw * 8, cudaMemcpyDeviceToDevice, D.st));
+    }
+    if ((rc = upload_luts_b(B, tsh))) return rc;
+    if ((rc = pbs_b(B, mbk, S, k, k, ids))) return rc;
+  }
+  // (6) packed index and (7) the 8-bit digit PBS
+  for (uint32_t i = 0; i < k; i++)
+    if ((rc = launch_lwe_axpy_bcast(packed + (size_t)i * count * cw, eB, 1, dB + (size_t)i * count * cw, 1,
+                                    S + (size_t)i * cw, 1, count, (int)(cw - 1), D.st)))
+      return rc;
+  {
+    std::vector<std::vector<u64>> tc = {table_window_b(0, [g](int x) {
+      const int neg = x >> 7, s = ((x >> 4) & 7) - 4, d = x & 15;
+      const int l = s < 0 ? 0 : (s > g - 1 ? g - 1 : s), r = s < 0 ? -s : 0;
+      const int val = (d << l) >> r;
+      return enc(neg ? -val : val, kDelta);
+    })};
+    if ((rc = upload_luts_b(B, tc))) return rc;
+    if ((rc = pbs_b(B, packed, R, (size_t)k * count, 1, {}))) return rc;
+  }
+  // (8) sum over digits
+  SZ_CUDA_OK(cudaMemcpyAsync(out, R, count * cw * 8, cudaMemcpyDeviceToDevice, D.st));
+  for (uint32_t i = 1; i < k; i++)
+    if ((rc = axpy3(D, out, out, 1, R + (size_t)i * count * cw, 1, nullptr, 0, 0, count))) return rc;
+  return SILENZIO_OK;
+}
+
+}  // extern "C"

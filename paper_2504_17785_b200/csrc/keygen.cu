@@ -170,6 +170,18 @@ __global__ void lwe_axpy3_kernel(u64 *out, const u64 *A, i64 ca, const u64 *B, i
   }
 }
 
+// out[e] = ca A[e] + cb B[e] + cc C[e mod (dim+1)]: C is ONE ciphertext broadcast to all
+__global__ void lwe_axpy_bcast_kernel(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc,
+                                      long count, int dim) {
+  const long total = count * (long)(dim + 1);
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    u64 s = (u64)cc * C[e % (dim + 1)];
+    if (A) s += (u64)ca * A[e];
+    if (B) s += (u64)cb * B[e];
+    out[e] = s;
+  }
+}
+
 // ------------------------------------------------------------ host launch
 int launch_lwe_encrypt(const u64 *mask, const i64 *noise, const u64 *pt, const u64 *key, int dim,
                        size_t count, u64 *out, cudaStream_t st) {
@@ -236,6 +248,17 @@ int launch_lwe_axpy3(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const
   long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   lwe_axpy3_kernel<<<(unsigned)blocks, 256, 0, st>>>(out, A, ca, B, cb, C, cc, cst, (long)count, dim);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+int launch_lwe_axpy_bcast(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc, size_t count,
+                          int dim, cudaStream_t st) {
+  if (count == 0) return SILENZIO_OK;
+  const long total = (long)count * (dim + 1);
+  long blocks = (total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  lwe_axpy_bcast_kernel<<<(unsigned)blocks, 256, 0, st>>>(out, A, ca, B, cb, C, cc, (long)count, dim);
   SZ_LAUNCH_OK();
   return SILENZIO_OK;
 }

@@ -64,6 +64,8 @@ def load():
         "silenzio_rns_sign_abs": ([V, V, U32, S, V, V, V, V, P, V, S, V], I),
         "silenzio_mrns_bitlen_max": ([V, U32, S, V, V, V, V, P, V, S, V], I),
         "silenzio_int_ce_grad": ([V, V, U32, U32, V, V, V, P, V, S, V], I),
+        "silenzio_mrns_combine_workspace_bytes": ([P, P, U32, S], S),
+        "silenzio_mrns_digit_combine": ([V, V, V, U32, S, U32, U32, U32, V, V, V, V, P, V, P, V, P, V, P, V, S, V], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -83,6 +85,7 @@ def exported_symbols():
         "silenzio_bsk_generate", "silenzio_bsk_generate_workspace_bytes", "silenzio_ksk_generate", "silenzio_rns_matmul_workspace_bytes",
         "silenzio_rns_matmul", "silenzio_gadget_workspace_bytes", "silenzio_rns2mrns",
         "silenzio_rns_sign_abs", "silenzio_mrns_bitlen_max", "silenzio_int_ce_grad",
+        "silenzio_mrns_combine_workspace_bytes", "silenzio_mrns_digit_combine",
     ]
 
 
@@ -336,3 +339,26 @@ def int_ce_grad(Yhat, Y, fourier_bsk, ksk, P, stream=None):
     _check(load().silenzio_int_ce_grad(_ptr(Yhat), _ptr(Y), a, b, _ptr(out), _ptr(fourier_bsk), _ptr(ksk),
                                        ctypes.byref(make_params(P)), _ptr(ws), ws.numel(), _stream(stream)))
     return out
+
+
+def ks_params(in_dim, out_dim, base_log, level, like):
+    """silenzio_params for a cross-parameter keyswitch (only the KS fields matter)."""
+    p = make_params(like)
+    p.ks_in_dim, p.lwe_dim, p.ks_base_log, p.ks_level = in_dim, out_dim, base_log, level
+    return p
+
+
+def mrns_digit_combine(top_digit, abs_digits, maxes, top_radix, w, gamma, keys_a, Pa, keys_b, Pb,
+                       ksk_ab, pab, ksk_ba, pba, stream=None):
+    """g7: Shift2MSBs+- output [count] and encrypted maxBit via the 8-bit (set B) stage."""
+    k, count = int(abs_digits.shape[0]), int(abs_digits.shape[1])
+    out = torch.empty((count, abs_digits.shape[-1]), dtype=torch.int64, device=abs_digits.device)
+    mb = torch.empty((1, abs_digits.shape[-1]), dtype=torch.int64, device=abs_digits.device)
+    pa, pb = make_params(Pa), make_params(Pb)
+    nb = load().silenzio_mrns_combine_workspace_bytes(ctypes.byref(pa), ctypes.byref(pb), k, count)
+    ws = torch.empty(nb, dtype=torch.uint8, device=abs_digits.device)
+    _check(load().silenzio_mrns_digit_combine(
+        _ptr(top_digit), _ptr(abs_digits), _ptr(maxes), k, count, top_radix, w, gamma, _ptr(out), _ptr(mb),
+        _ptr(keys_a["fbsk"]), _ptr(keys_a["ksk"]), ctypes.byref(pa), _ptr(keys_b["fbsk"]), ctypes.byref(pb),
+        _ptr(ksk_ab), ctypes.byref(pab), _ptr(ksk_ba), ctypes.byref(pba), _ptr(ws), ws.numel(), _stream(stream)))
+    return out, mb

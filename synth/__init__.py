@@ -15,4 +15,5 @@ from .inputs import (  # noqa: F401
     lut_ids,
     streams,
     config0_table,
+    cross_ksk_randomness,
 )

@@ -93,3 +93,12 @@ def config0_table(p: int = 4) -> np.ndarray:
     """BASELINE configs[0]: f(x) = (3x + 1) mod 16, the workload definition."""
     x = np.arange(1 << p, dtype=np.int64)
     return ((3 * x + 1) % (1 << p)).reshape(1, -1)
+
+
+def cross_ksk_randomness(in_dim: int, level: int, n_out: int, sigma_log2: float, seed: int, tag: int) -> dict:
+    """Masks and noise of a keyswitching key between two parameter sets
+    (config 4: set-A big key -> set-B small key, set-B big key -> set-A big key).
+    Own stream: SeedSequence((seed, 1000 + tag))."""
+    rng = np.random.Generator(np.random.PCG64(np.random.SeedSequence([seed, 1000 + tag])))
+    return {"ksk_mask": _uniform_u64(rng, (in_dim, level, n_out)),
+            "ksk_noise": _gaussian_i64(rng, (in_dim, level), sigma_log2)}
