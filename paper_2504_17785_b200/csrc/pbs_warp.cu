@@ -1,0 +1,548 @@
+// pbs_warp.cu -- blind rotation for k = 1, N = 2048, level-1 gadget (parameter
+// set A, the benchmark configuration) with warp-synchronous FFTs, the
+// accumulator and the digit spectra in tensor memory, and the Fourier BSK
+// staged into shared memory by the bulk-copy (TMA) engine.
+//
+// Same method and conventions as pbs.cu (SURVEY.md §8(a) a2-a5, §8(c) C4-C7,
+// DESIGN.md R3-R6, R20); only the data movement differs:
+//
+//  * FFT: M = 1024 = 32 x 32 complex points per transform, one warp per
+//    transform, 32 values per thread: pass 1 (radix 32 in registers), one
+//    transposition through shared memory (XOR-swizzled, conflict free),
+//    pass 2 (radix 32). Only __syncwarp between passes.
+//  * CTA = 8 warps = 4 ciphertexts; ciphertext s uses warp s (GLWE mask
+//    component) and warp s + 4 (body). Both warps of a ciphertext access the
+//    same TMEM lane quadrant, so a thread and its partner share one lane:
+//      columns [  0,128)  ACC_0 (warp s),  [128,256) ACC_1 (warp s + 4)
+//      columns [256,384)  D^_0 (row 0 spectrum), [384,512) D^_1
+//    The MAC reads both digit spectra from TMEM (off the L1/shared path).
+//  * The four ciphertexts of a CTA run the CMux loop in lock step and share
+//    the Fourier BSK: one 64 KiB bulk copy per (i, limb) into shared memory,
+//    issued by one thread right after the previous limb's MAC and landing
+//    during the inverse FFT (mbarrier completion).
+//
+// Fourier BSK layout for this kernel: [n][P][2 (o)][2 (row)][32 (r)][32 (lane)]
+// where (r, lane) holds the spectrum at index lane + 32 bitrev5(r), times 1/M.
+#include <cmath>
+#include <mutex>
+
+#include "fft.cuh"
+#include "limbs.cuh"
+#include "tmem.cuh"
+
+namespace sz {
+namespace w32 {
+
+constexpr int kN = 2048;
+constexpr int kLog2_2N = 12;
+constexpr int kM = 1024;
+constexpr int kCts = 4;       // ciphertexts per CTA
+constexpr int kThreads = 256;  // 8 warps
+constexpr uint32_t kTmemCols = 512;
+
+// cos(2 pi e / 32), e = 0..31 (correctly rounded doubles)
+struct C32 {
+  static constexpr double c[32] = {
+      1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452, 0.7071067811865476, 0.5555702330196022,
+      0.3826834323650898, 0.19509032201612828, 0.0, -0.19509032201612828, -0.3826834323650898,
+      -0.5555702330196022, -0.7071067811865476, -0.8314696123025452, -0.9238795325112867, -0.9807852804032304,
+      -1.0, -0.9807852804032304, -0.9238795325112867, -0.8314696123025452, -0.7071067811865476,
+      -0.5555702330196022, -0.3826834323650898, -0.19509032201612828, 0.0, 0.19509032201612828,
+      0.3826834323650898, 0.5555702330196022, 0.7071067811865476, 0.8314696123025452, 0.9238795325112867,
+      0.9807852804032304};
+};
+
+// multiply by W_32^E = e^{+2 pi i E / 32} (conjugate when INV)
+template <int E, bool INV>
+__device__ __forceinline__ double2 mulw32(double2 a) {
+  constexpr int e = INV ? ((32 - (E & 31)) & 31) : (E & 31);
+  if constexpr (e == 0) {
+    return a;
+  } else if constexpr (e == 8) {
+    return make_double2(-a.y, a.x);
+  } else if constexpr (e == 16) {
+    return make_double2(-a.x, -a.y);
+  } else if constexpr (e == 24) {
+    return make_double2(a.y, -a.x);
+  } else {
+    constexpr double c = C32::c[e];
+    constexpr double s = C32::c[(e + 24) & 31];  // sin(2 pi e/32) = cos(2 pi (e-8)/32)
+    return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
+  }
+}
+
+template <bool INV>
+__device__ __forceinline__ double2 mulw32v(double2 d, int e) {
+  switch (e & 31) {
+#define SZ_W(k) \
+  case k: return mulw32<k, INV>(d);
+    SZ_W(0) SZ_W(1) SZ_W(2) SZ_W(3) SZ_W(4) SZ_W(5) SZ_W(6) SZ_W(7)
+    SZ_W(8) SZ_W(9) SZ_W(10) SZ_W(11) SZ_W(12) SZ_W(13) SZ_W(14) SZ_W(15)
+#undef SZ_W
+    default: return d;
+  }
+}
+
+// In-place radix-2 DIF DFT of size 32 on registers, exponent sign + (conjugate
+// when INV). Natural-order input, bit-reversed output: x[r] = X[bitrev5(r)].
+template <bool INV, int H>
+__device__ __forceinline__ void dft32_stage(double2 (&x)[32]) {
+  if constexpr (H >= 1) {
+#pragma unroll
+    for (int b = 0; b < 32; b += 2 * H)
+#pragma unroll
+      for (int j = 0; j < H; j++) {
+        const double2 a = x[b + j], c = x[b + j + H];
+        x[b + j] = cadd(a, c);
+        x[b + j + H] = mulw32v<INV>(csub(a, c), j * (16 / H));  // W_{2H}^j = W_32^{j 32/(2H)}
+      }
+    dft32_stage<INV, H / 2>(x);
+  }
+}
+template <bool INV>
+__device__ __forceinline__ void dft32(double2 (&x)[32]) {
+  dft32_stage<INV, 16>(x);
+}
+
+__host__ __device__ constexpr int bitrev5(int r) {
+  return ((r & 1) << 4) | ((r & 2) << 2) | (r & 4) | ((r & 8) >> 2) | ((r & 16) >> 4);
+}
+
+// Tables (host-built in long double, rounded once), w = e^{i pi / 2048}:
+//   tw [k1 * 32 + l] = w^{l (1 + 4 k1)}  (negacyclic twist w^l folded with the
+//   twT[l * 32 + k1] = same value         four-step twiddle e^{2 pi i l k1 / M})
+//   c_twist32[m]     = w^{32 m} = e^{i pi m / 64}
+struct Tables32 {
+  double2 tw[32 * 32];
+  double2 twT[32 * 32];
+};
+__device__ Tables32 g_t32;
+__constant__ double2 c_twist32[32];
+
+static std::once_flag g_once[64];
+static int g_status[64];
+
+static int init_tables(int dev) {
+  static Tables32 h;
+  double2 tws[32];
+  const long double PI = 3.141592653589793238462643383279502884L;
+  for (int k1 = 0; k1 < 32; k1++)
+    for (int l = 0; l < 32; l++) {
+      const long double ang = PI * (long double)(l * (1 + 4 * k1)) / 2048.0L;
+      const double2 v = make_double2((double)cosl(ang), (double)sinl(ang));
+      h.tw[k1 * 32 + l] = v;
+      h.twT[l * 32 + k1] = v;
+    }
+  for (int m = 0; m < 32; m++) {
+    const long double ang = PI * (long double)m / 64.0L;
+    tws[m] = make_double2((double)cosl(ang), (double)sinl(ang));
+  }
+  int prev = 0;
+  if (cudaGetDevice(&prev) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  if (prev != dev && cudaSetDevice(dev) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  cudaError_t e = cudaMemcpyToSymbol(g_t32, &h, sizeof(Tables32));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_twist32, tws, sizeof(tws));
+  if (prev != dev) cudaSetDevice(prev);
+  return e == cudaSuccess ? SILENZIO_OK : SILENZIO_ERR_CUDA;
+}
+
+static int ensure_tables() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return SILENZIO_ERR_CUDA;
+  std::call_once(g_once[dev], [dev] { g_status[dev] = init_tables(dev); });
+  return g_status[dev];
+}
+
+// swizzled index of element (row, col) of a 32 x 32 block of 16-byte values:
+// any 8 consecutive rows (fixed col) or cols (fixed row) hit 8 distinct 16-byte bank groups
+__device__ __forceinline__ int sw(int row, int col) { return row * 32 + (col ^ (row & 7)); }
+
+// Forward transform of one warp. In: x[m] = (a_j + i a_{j+1024}) at j = lane + 32 m.
+// Out: x[r] = spectrum at index lane + 32 bitrev5(r) ("slot" order).
+__device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, int lane) {
+#pragma unroll
+  for (int m = 1; m < 32; m++) x[m] = cmul(x[m], c_twist32[m]);
+  dft32<false>(x);  // x[r] = B[l = lane][k1 = bitrev5(r)]
+  __syncwarp();     // earlier readers of buf are done
+#pragma unroll
+  for (int r = 0; r < 32; r++) {
+    const int k1 = bitrev5(r);
+    buf[sw(lane, k1)] = cmul(x[r], __ldg(&g_t32.tw[k1 * 32 + lane]));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int l = 0; l < 32; l++) x[l] = buf[sw(l, lane)];  // thread k1 = lane, natural l
+  dft32<false>(x);
+}
+
+// Inverse transform (unnormalised). In: slot order. Out: x[m] = M (c_j + i c_{j+1024}), j = lane + 32 m.
+__device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, int lane) {
+  double2 z[32];
+#pragma unroll
+  for (int r = 0; r < 32; r++) z[bitrev5(r)] = x[r];  // natural k2
+  dft32<true>(z);                                     // z[r] = 32 B'[l = bitrev5(r)][k1 = lane]
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 32; r++) {
+    const int l = bitrev5(r);
+    buf[sw(l, lane)] = cmulc(z[r], __ldg(&g_t32.twT[l * 32 + lane]));
+  }
+  __syncwarp();
+#pragma unroll
+  for (int k1 = 0; k1 < 32; k1++) z[k1] = buf[sw(lane, k1)];  // thread l = lane, natural k1
+  dft32<true>(z);                                             // z[r] = M z_{lane + 32 m} w^{32 m}, m = bitrev5(r)
+#pragma unroll
+  for (int r = 0; r < 32; r++) {
+    const int m = bitrev5(r);
+    x[m] = (m == 0) ? z[r] : cmulc(z[r], c_twist32[m]);
+  }
+}
+
+// ------------------------------------------------------------ mbarrier / bulk copy
+__device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SZ_WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SZ_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(mbar)),
+      "r"(phase)
+      : "memory");
+}
+// arm the barrier for `bytes` and bulk-copy them global -> shared (one thread)
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *mbar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+
+// ------------------------------------------------------------------ kernel
+struct Args {
+  const u64 *lwe_small;  // [count][n+1]
+  const u32 *lut_ids;    // [count] or null
+  const u64 *luts;       // [num_luts][N]
+  u32 num_luts;
+  const double2 *fbsk;   // [n][P][2][2][32][32]
+  u64 *lwe_out;          // [count][N+1]
+  long count;
+  int n, base_log, w;
+};
+
+__host__ __device__ constexpr size_t abar_bytes(int n) { return ((size_t)n * 2 + 15) / 16 * 16; }
+__host__ __device__ constexpr size_t smem_bytes(int n) {
+  return 8 * (size_t)kM * sizeof(double2)    // per-warp transposition buffers (also the ACC copy)
+         + 4 * (size_t)kM * sizeof(double2)  // BSK stage: one (i, limb), [o][row][32][32]
+         + kCts * abar_bytes(n)              // modswitched masks
+         + 16;                               // mbarrier
+}
+
+__device__ __forceinline__ u64 acc_init(const u64 *v, int j, int bt, int g) {
+  const int idx = (j + bt) & (2 * kN - 1);
+  const u64 vv = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
+  return g ? vv : 0ull;
+}
+// ACC chunk cc (16 columns) = coefficients j = lane + 32 m + 1024 h, m = 4 cc + q (q < 4), h < 2
+__device__ __forceinline__ void acc_ld(uint32_t ta, int cc, u64 (&a)[4][2]) {
+  uint32_t r[16];
+  tmem_ld16(ta + 16 * cc, r);
+  tmem_wait_ld16(r);
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) a[q][h] = (u64)r[4 * q + 2 * h] | ((u64)r[4 * q + 2 * h + 1] << 32);
+}
+__device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[4][2]) {
+  uint32_t r[16];
+#pragma unroll
+  for (int q = 0; q < 4; q++)
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+      r[4 * q + 2 * h] = (uint32_t)a[q][h];
+      r[4 * q + 2 * h + 1] = (uint32_t)(a[q][h] >> 32);
+    }
+  tmem_st16(ta + 16 * cc, r);
+}
+
+template <int P>
+__global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t tmem_slot;
+  const int n = A.n, w = A.w, blog = A.base_log;
+  double2 *xbuf_all = reinterpret_cast<double2 *>(smem);
+  double2 *gbuf = xbuf_all + 8 * kM;
+  unsigned char *abar_base = reinterpret_cast<unsigned char *>(gbuf + 4 * kM);
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(abar_base + kCts * abar_bytes(n));
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  const int cs = wid & 3, g = wid >> 2;  // ciphertext slot, GLWE component
+  double2 *xbuf = xbuf_all + wid * kM;
+  u64 *accs = reinterpret_cast<u64 *>(xbuf);  // ACC_g copy [2048] for the rotation
+  unsigned short *abar = reinterpret_cast<unsigned short *>(abar_base + cs * abar_bytes(n));
+
+  if (wid == 0) tmem_alloc(&tmem_slot, kTmemCols);
+  if (tid == 32) mbar_init(mbar, 1);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tl = tmem_slot + ((uint32_t)(32 * cs) << 16);
+  const uint32_t ta_acc = tl + 128 * g, ta_d0 = tl + 256, ta_d1 = tl + 384, ta_dg = tl + 256 + 128 * g;
+  const uint32_t limb_bytes = 4 * kM * sizeof(double2);
+  auto issue = [&](int i, int p) {
+    bulk_load(gbuf, A.fbsk + ((size_t)i * P + p) * 4 * kM, limb_bytes, mbar);
+  };
+  uint32_t round = 0;  // completed bulk copies (mbarrier phase parity)
+
+  const long ngroups = (A.count + kCts - 1) / kCts;
+  for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    if (tid == 0) issue(0, P - 1);
+    const long c_raw = grp * kCts + cs;
+    const bool live = c_raw < A.count;
+    const long c = live ? c_raw : A.count - 1;  // idle slots replay the last ciphertext
+    const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
+    // ---- modulus switch (a2)
+    for (int i = g * 32 + lane; i < n; i += 64) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2N);
+    const int bt = (int)sz_modswitch(lwe[n], kLog2_2N);
+    // ---- ACC init (a3): ACC = (0, X^{-b~} v)
+    u32 id = A.lut_ids ? A.lut_ids[c] : 0u;
+    if (id >= A.num_luts) id = 0;
+    const u64 *v = A.luts + (size_t)id * kN;
+#pragma unroll 1
+    for (int cc = 0; cc < 8; cc++) {
+      u64 a4[4][2];
+#pragma unroll
+      for (int q = 0; q < 4; q++)
+#pragma unroll
+        for (int h = 0; h < 2; h++) a4[q][h] = acc_init(v, lane + 32 * (4 * cc + q) + 1024 * h, bt, g);
+      acc_st(ta_acc, cc, a4);
+    }
+    tmem_wait_st();
+    __syncthreads();  // abar visible
+
+    for (int i = 0; i < n; i++) {
+      const int a = abar[i];
+      // ---------------- publish ACC_g for the rotation
+      __syncwarp();  // previous inverse FFT's readers of xbuf are done
+#pragma unroll
+      for (int cc = 0; cc < 8; cc++) {
+        u64 a4[4][2];
+        acc_ld(ta_acc, cc, a4);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) accs[lane + 32 * (4 * cc + q) + 1024 * h] = a4[q][h];
+      }
+      __syncwarp();
+      // ---------------- digits of X^a ACC_g - ACC_g (a4.1-a4.2), forward FFT
+      double2 x[32];
+#pragma unroll
+      for (int cc = 0; cc < 8; cc++) {
+        u64 a4[4][2];
+        acc_ld(ta_acc, cc, a4);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          double dv[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int j = lane + 32 * (4 * cc + q) + 1024 * h;
+            const int src = (j - a) & (2 * kN - 1);
+            const u64 rv = accs[src & (kN - 1)];
+            const u64 rot = (src < kN) ? rv : (u64)0 - rv;
+            u64 r = sz_decomp_round(rot - a4[q][h], blog, 1);
+            dv[h] = (double)sz_decomp_next(r, blog);
+          }
+          x[4 * cc + q] = make_double2(dv[0], dv[1]);
+        }
+      }
+      fwd_fft32(x, xbuf, lane);
+#pragma unroll
+      for (int jj = 0; jj < 8; jj++) {
+        uint32_t r16[16];
+        pack4(&x[4 * jj], r16);
+        tmem_st16(ta_dg + 16 * jj, r16);
+      }
+      tmem_wait_st();
+      tmem_fence_before();
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + cs), "r"(64) : "memory");  // D^_0 and D^_1 written
+      tmem_fence_after();
+      // ---------------- per limb: MAC with the staged BSK, inverse FFT, exact ACC update
+#pragma unroll 1
+      for (int p = P - 1; p >= 0; p--) {
+        mbar_wait(mbar, round & 1);
+        round++;
+        double2 y[32];
+        const double2 *G0 = gbuf + (size_t)(2 * g) * kM + lane;  // [o = g][row 0]
+        const double2 *G1 = G0 + kM;                             // [o = g][row 1]
+#pragma unroll
+        for (int jj = 0; jj < 8; jj++) {
+          uint32_t d0[16], d1[16];
+          tmem_ld16(ta_d0 + 16 * jj, d0);
+          tmem_ld16(ta_d1 + 16 * jj, d1);
+          tmem_wait_ld16x2(d0, d1);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int r = 4 * jj + q;
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, unpack1(d0, q), G0[r * 32]);
+            cmac(acc, unpack1(d1, q), G1[r * 32]);
+            y[r] = acc;
+          }
+        }
+        tmem_fence_before();
+        __syncthreads();  // every warp is done with gbuf (and, for p = 0, with D^)
+        tmem_fence_after();
+        if (tid == 0) {
+          if (p > 0) issue(i, p - 1);
+          else if (i + 1 < n) issue(i + 1, P - 1);
+        }
+        inv_fft32(y, xbuf, lane);
+#pragma unroll
+        for (int cc = 0; cc < 8; cc++) {
+          u64 a4[4][2];
+          acc_ld(ta_acc, cc, a4);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            a4[q][0] += limb_to_torus(y[4 * cc + q].x, p, P, w);
+            a4[q][1] += limb_to_torus(y[4 * cc + q].y, p, P, w);
+          }
+          acc_st(ta_acc, cc, a4);
+        }
+        tmem_wait_st();
+      }
+    }
+    // ---- sample extraction (a5): a'[0] = A[0], a'[i] = -A[N-i], b' = B[0]
+    if (live) {
+      u64 *out = A.lwe_out + (size_t)c * (kN + 1);
+#pragma unroll 1
+      for (int cc = 0; cc < 8; cc++) {
+        u64 a4[4][2];
+        acc_ld(ta_acc, cc, a4);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            const int j = lane + 32 * (4 * cc + q) + 1024 * h;
+            if (g == 0) {
+              if (j == 0) out[0] = a4[q][h];
+              else out[kN - j] = (u64)0 - a4[q][h];
+            } else if (j == 0) {
+              out[kN] = a4[q][h];
+            }
+          }
+      }
+    }
+    __syncthreads();  // abar reuse
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (wid == 0) tmem_dealloc(tmem_slot, kTmemCols);
+}
+
+// --------------------------------------------------------- BSK -> Fourier
+struct B2FArgs {
+  const u64 *bsk;  // [n][2 (rows)][2 (o)][N]
+  double2 *fbsk;   // [n][P][2 (o)][2 (row)][32][32]
+  int n, P, w;
+};
+
+// one warp per (i, row, o, p)
+__global__ void __launch_bounds__(32) bsk_to_fourier_warp_kernel(B2FArgs A) {
+  __shared__ __align__(16) double2 buf[kM];
+  const int lane = threadIdx.x;
+  long blk = blockIdx.x;
+  const int p = blk % A.P; blk /= A.P;
+  const int o = blk % 2; blk /= 2;
+  const int row = blk % 2; blk /= 2;
+  const int i = (int)blk;
+  const u64 *gsrc = A.bsk + (((size_t)i * 2 + row) * 2 + o) * kN;
+  double2 x[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    double l0[3], l1[3];
+    limb_split(gsrc[lane + 32 * m], A.P, A.w, l0);
+    limb_split(gsrc[lane + 32 * m + 1024], A.P, A.w, l1);
+    x[m] = make_double2(l0[p], l1[p]);
+  }
+  fwd_fft32(x, buf, lane);
+  double2 *dst = A.fbsk + ((((size_t)i * A.P + p) * 2 + o) * 2 + row) * kM;
+  const double scale = 1.0 / kM;
+#pragma unroll
+  for (int r = 0; r < 32; r++) dst[r * 32 + lane] = make_double2(x[r].x * scale, x[r].y * scale);
+}
+
+}  // namespace w32
+
+// ------------------------------------------------------------------ host side
+bool blind_rotate_warp_supported(const silenzio_params *P) {
+  return P->poly_size == 2048 && P->glwe_dim == 1 && P->pbs_level == 1 && P->fft_limbs >= 1 && P->fft_limbs <= 3 &&
+         w32::smem_bytes((int)P->lwe_dim) <= 227 * 1024;
+}
+
+long blind_rotate_warp_wave() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return (long)sms * w32::kCts;  // one CTA (4 ciphertexts) per SM: 512 TMEM columns each
+}
+
+int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
+                             const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
+                             cudaStream_t stream) {
+  int st = w32::ensure_tables();
+  if (st != SILENZIO_OK) return st;
+  void (*kern)(w32::Args) = nullptr;
+  if (P->fft_limbs == 1) kern = w32::blind_rotate_warp_kernel<1>;
+  if (P->fft_limbs == 2) kern = w32::blind_rotate_warp_kernel<2>;
+  if (P->fft_limbs == 3) kern = w32::blind_rotate_warp_kernel<3>;
+  if (!kern) return SILENZIO_ERR_UNSUPPORTED;
+  w32::Args A;
+  A.lwe_small = lwe_small;
+  A.lut_ids = lut_ids;
+  A.luts = luts;
+  A.num_luts = num_luts;
+  A.fbsk = reinterpret_cast<const double2 *>(fbsk);
+  A.lwe_out = lwe_out;
+  A.count = (long)count;
+  A.n = (int)P->lwe_dim;
+  A.base_log = (int)P->pbs_base_log;
+  A.w = (int)P->limb_bits;
+  const size_t smem = w32::smem_bytes(A.n);
+  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const long wave = blind_rotate_warp_wave();
+  if (wave <= 0) return SILENZIO_ERR_CUDA;
+  // one launch per resident wave (every CTA sweeps BSK_0..BSK_{n-1} together)
+  for (long c0 = 0; c0 < (long)count; c0 += wave) {
+    w32::Args W = A;
+    const long cnt = ((long)count - c0 < wave) ? (long)count - c0 : wave;
+    W.lwe_small = A.lwe_small + (size_t)c0 * (A.n + 1);
+    W.lut_ids = A.lut_ids ? A.lut_ids + c0 : nullptr;
+    W.lwe_out = A.lwe_out + (size_t)c0 * (w32::kN + 1);
+    W.count = cnt;
+    kern<<<(unsigned)((cnt + w32::kCts - 1) / w32::kCts), w32::kThreads, smem, stream>>>(W);
+    SZ_LAUNCH_OK();
+  }
+  return SILENZIO_OK;
+}
+
+int launch_bsk_to_fourier_warp(const u64 *bsk, void *fbsk, const silenzio_params *P, cudaStream_t stream) {
+  int st = w32::ensure_tables();
+  if (st != SILENZIO_OK) return st;
+  w32::B2FArgs A;
+  A.bsk = bsk;
+  A.fbsk = reinterpret_cast<double2 *>(fbsk);
+  A.n = (int)P->lwe_dim;
+  A.P = (int)P->fft_limbs;
+  A.w = (int)P->limb_bits;
+  const long blocks = (long)A.n * 2 * 2 * A.P;
+  w32::bsk_to_fourier_warp_kernel<<<(unsigned)blocks, 32, 0, stream>>>(A);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+}  // namespace sz
