@@ -43,4 +43,13 @@ __device__ __forceinline__ u64 limb_to_torus(double x, int p, int P, int w) {
   return f64_to_torus(x);                                          // P <= 2, low limb may exceed 2^53
 }
 
+// Exact round-to-nearest (ties to even, as F2I.RN) of a double with |x| < 2^51,
+// as a two's-complement u64, on the FP64 pipe: adding 1.5 * 2^52 leaves
+// round(x) in the low mantissa bits. The P = 3 limb sums stay below 2^51 with
+// overwhelming margin (R20: sigma ~ 2^47.4, 2^51 is > 11 sigma).
+__device__ __forceinline__ u64 rint_small(double x) {
+  const double magic = 6755399441055744.0;  // 1.5 * 2^52
+  return (u64)(__double_as_longlong(x + magic) - __double_as_longlong(magic));
+}
+
 }  // namespace sz

@@ -298,6 +298,9 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
     bulk_load(gbuf, A.fbsk + ((size_t)i * P + p) * 4 * kM, limb_bytes, mbar);
   };
   uint32_t round = 0;  // completed bulk copies (mbarrier phase parity)
+  const u64 half_q = 1ull << (63 - blog);
+  __shared__ int mac_done;  // warps finished with the staged limb (the last one re-arms the stage)
+  if (tid == 0) mac_done = 0;
 
   const long ngroups = (A.count + kCts - 1) / kCts;
   for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
@@ -354,13 +357,20 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
             const int src = (j - a) & (2 * kN - 1);
             const u64 rv = accs[src & (kN - 1)];
             const u64 rot = (src < kN) ? rv : (u64)0 - rv;
-            u64 r = sz_decomp_round(rot - a4[q][h], blog, 1);
-            dv[h] = (double)sz_decomp_next(r, blog);
+            // level-1 balanced digit round((rot - acc) B / q) in [-B/2, B/2): the
+            // arithmetic shift of the half-up-rounded value (C3; the carry out of
+            // the only level is dropped, as in sz_decomp_next)
+            dv[h] = (double)((i64)(rot - a4[q][h] + half_q) >> (64 - blog));
           }
           x[4 * cc + q] = make_double2(dv[0], dv[1]);
         }
       }
       fwd_fft32(x, xbuf, lane);
+      if (i > 0) {  // both warps of the ciphertext are past the previous CMux's MACs (D^ reads)
+        tmem_fence_before();
+        asm volatile("bar.sync %0, %1;" ::"r"(5 + cs), "r"(64) : "memory");
+        tmem_fence_after();
+      }
 #pragma unroll
       for (int jj = 0; jj < 8; jj++) {
         uint32_t r16[16];
@@ -380,26 +390,29 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
         const double2 *G0 = gbuf + (size_t)(2 * g) * kM + lane;  // [o = g][row 0]
         const double2 *G1 = G0 + kM;                             // [o = g][row 1]
 #pragma unroll
-        for (int jj = 0; jj < 8; jj++) {
-          uint32_t d0[16], d1[16];
-          tmem_ld16(ta_d0 + 16 * jj, d0);
-          tmem_ld16(ta_d1 + 16 * jj, d1);
-          tmem_wait_ld16x2(d0, d1);
+        for (int jj = 0; jj < 4; jj++) {
+          uint32_t d0[32], d1[32];
+          tmem_ld32(ta_d0 + 32 * jj, d0);
+          tmem_ld32(ta_d1 + 32 * jj, d1);
+          tmem_wait_ld32x2(d0, d1);
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const int r = 4 * jj + q;
+          for (int q = 0; q < 8; q++) {
+            const int r = 8 * jj + q;
             double2 acc = make_double2(0.0, 0.0);
             cmac(acc, unpack1(d0, q), G0[r * 32]);
             cmac(acc, unpack1(d1, q), G1[r * 32]);
             y[r] = acc;
           }
         }
-        tmem_fence_before();
-        __syncthreads();  // every warp is done with gbuf (and, for p = 0, with D^)
-        tmem_fence_after();
-        if (tid == 0) {
-          if (p > 0) issue(i, p - 1);
-          else if (i + 1 < n) issue(i + 1, P - 1);
+        // this warp is done with the stage; the last of the 8 warps re-arms it
+        // with the next (i, limb) -- no CTA-wide barrier
+        __syncwarp();
+        if (lane == 0) {
+          if (atomicAdd(&mac_done, 1) == kThreads / 32 - 1) {
+            mac_done = 0;
+            if (p > 0) issue(i, p - 1);
+            else if (i + 1 < n) issue(i + 1, P - 1);
+          }
         }
         inv_fft32(y, xbuf, lane);
 #pragma unroll
@@ -408,8 +421,13 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
           acc_ld(ta_acc, cc, a4);
 #pragma unroll
           for (int q = 0; q < 4; q++) {
-            a4[q][0] += limb_to_torus(y[4 * cc + q].x, p, P, w);
-            a4[q][1] += limb_to_torus(y[4 * cc + q].y, p, P, w);
+            if (P == 3) {
+              a4[q][0] += rint_small(y[4 * cc + q].x) << (p * w);
+              a4[q][1] += rint_small(y[4 * cc + q].y) << (p * w);
+            } else {
+              a4[q][0] += limb_to_torus(y[4 * cc + q].x, p, P, w);
+              a4[q][1] += limb_to_torus(y[4 * cc + q].y, p, P, w);
+            }
           }
           acc_st(ta_acc, cc, a4);
         }
