@@ -20,6 +20,8 @@ int launch_bsk_to_fourier_huge(const u64 *, void *, const silenzio_params *, cud
 size_t blind_rotate_huge_ws_bytes(const silenzio_params *, size_t);
 long blind_rotate_huge_wave(const silenzio_params *);
 int launch_keyswitch(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, cudaStream_t);
+size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log);
+int launch_keyswitch_tc(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, void *, cudaStream_t);
 int launch_lwe_encrypt(const u64 *, const i64 *, const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_lwe_phase(const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_bsk_generate(const u64 *, const u64 *, const u64 *, const i64 *, u64 *, int, int, int, int, int,
@@ -116,9 +118,28 @@ size_t silenzio_blind_rotate_workspace_bytes(const silenzio_params *P, size_t co
   return 0;
 }
 
+size_t silenzio_keyswitch_workspace_bytes(const silenzio_params *P, size_t count) {
+  (void)count;
+  if (check_params(P) != SILENZIO_OK || check_ks_params(P) != SILENZIO_OK) return 0;
+  return round_up(keyswitch_tc_workspace_bytes((int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_level,
+                                               (int)P->ks_base_log), 256);
+}
+
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *P, size_t count) {
   if (check_params(P) != SILENZIO_OK) return 0;
-  return round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256) + silenzio_blind_rotate_workspace_bytes(P, count);
+  return round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256) + silenzio_blind_rotate_workspace_bytes(P, count) +
+         silenzio_keyswitch_workspace_bytes(P, count);
+}
+
+// tensor-core keyswitch when the parameters allow it and a workspace is given,
+// else the CUDA-core kernel (both exact)
+static int run_keyswitch(const u64 *in, const u64 *ksk, u64 *out, size_t count, const silenzio_params *P,
+                         void *ks_ws, cudaStream_t st) {
+  if (ks_ws && silenzio_keyswitch_workspace_bytes(P, count) > 0)
+    return launch_keyswitch_tc(in, ksk, out, count, (int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_base_log,
+                               (int)P->ks_level, ks_ws, st);
+  return launch_keyswitch(in, ksk, out, count, (int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_base_log,
+                          (int)P->ks_level, st);
 }
 
 int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fbsk, const silenzio_params *P, void *stream) {
@@ -133,15 +154,15 @@ int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fbsk, const silenzio_para
 }
 
 int silenzio_keyswitch_batch(const uint64_t *in, const uint64_t *ksk, uint64_t *out, size_t count,
-                             const silenzio_params *P, void *stream) {
+                             const silenzio_params *P, void *workspace, void *stream) {
   int st = check_params(P);
   if (st) return st;
   if ((st = check_ks_params(P))) return st;
   if (count == 0) return SILENZIO_OK;
   if (!in || !ksk || !out) return SILENZIO_ERR_NULL_POINTER;
   if (count > (1ull << 36)) return SILENZIO_ERR_COUNT;
-  return launch_keyswitch(in, ksk, out, count, (int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_base_log,
-                          (int)P->ks_level, sz_stream(stream));
+  if (workspace && !sz_aligned16(workspace)) return SILENZIO_ERR_MISALIGNED;
+  return run_keyswitch(in, ksk, out, count, P, workspace, sz_stream(stream));
 }
 
 int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_ids, const uint64_t *luts,
@@ -175,11 +196,11 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
   if (!in || !luts || !fbsk || !ksk || !out) return SILENZIO_ERR_NULL_POINTER;
   if (!workspace) return SILENZIO_ERR_WORKSPACE;
   if (in == out) return SILENZIO_ERR_INVALID_PARAM;
+  if (!sz_aligned16(workspace)) return SILENZIO_ERR_MISALIGNED;
   u64 *small = reinterpret_cast<u64 *>(workspace);
-  if ((st = launch_keyswitch(in, ksk, small, count, (int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_base_log,
-                             (int)P->ks_level, sz_stream(stream))))
-    return st;
-  void *br_ws = reinterpret_cast<unsigned char *>(workspace) + round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256);
+  unsigned char *br_ws = reinterpret_cast<unsigned char *>(workspace) + round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256);
+  unsigned char *ks_ws = br_ws + silenzio_blind_rotate_workspace_bytes(P, count);
+  if ((st = run_keyswitch(in, ksk, small, count, P, ks_ws, sz_stream(stream)))) return st;
   return silenzio_blind_rotate_batch(small, lut_ids, luts, num_luts, fbsk, out, count, P, br_ws, stream);
 }
 

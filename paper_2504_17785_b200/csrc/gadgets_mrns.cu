@@ -275,7 +275,8 @@ int silenzio_int_ce_grad(const uint64_t *Yhat, const uint64_t *Y, uint32_t a, ui
 // A set-B PBS here = KS (set-A big key -> set-B small key) -> BR at N = 32768
 // -> SE (set-B big key) -> KS (set-B big key -> set-A big key).
 extern "C" {
-int silenzio_keyswitch_batch(const uint64_t *, const uint64_t *, uint64_t *, size_t, const silenzio_params *, void *);
+int silenzio_keyswitch_batch(const uint64_t *, const uint64_t *, uint64_t *, size_t, const silenzio_params *, void *,
+                             void *);
 int silenzio_blind_rotate_batch(const uint64_t *, const uint32_t *, const uint64_t *, uint32_t, const void *,
                                 uint64_t *, size_t, const silenzio_params *, void *, void *);
 size_t silenzio_blind_rotate_workspace_bytes(const silenzio_params *, size_t);
@@ -332,11 +333,11 @@ int pbs_b(DevB &B, const u64 *in, u64 *out, size_t count, u32 num_luts, const st
       SZ_CUDA_OK(cudaStreamSynchronize(B.st));
       idp = B.ids;
     }
-    int rc = silenzio_keyswitch_batch(in + c0 * ca, B.ksk_ab, B.small, cnt, B.pab, B.st);
+    int rc = silenzio_keyswitch_batch(in + c0 * ca, B.ksk_ab, B.small, cnt, B.pab, nullptr, B.st);
     if (rc) return rc;
     if ((rc = silenzio_blind_rotate_batch(B.small, idp, B.luts, num_luts, B.fbsk, B.big, cnt, B.pb, B.brws, B.st)))
       return rc;
-    if ((rc = silenzio_keyswitch_batch(B.big, B.ksk_ba, out + c0 * ca, cnt, B.pba, B.st))) return rc;
+    if ((rc = silenzio_keyswitch_batch(B.big, B.ksk_ba, out + c0 * ca, cnt, B.pba, nullptr, B.st))) return rc;
   }
   return SILENZIO_OK;
 }

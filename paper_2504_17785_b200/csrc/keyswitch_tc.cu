@@ -1,0 +1,324 @@
+// keyswitch_tc.cu -- batched LWE keyswitch on the 5th-generation tensor cores
+// (tcgen05.mma kind::i8, accumulators in TMEM), SURVEY.md §8(a) a1, §8(c) C3:
+//     out = (0,...,0,b) - sum_j sum_t Dec_t(a_j) * KSK[j][t]   mod 2^64.
+//
+// As a matrix product over the batch: D [count x K] (signed gadget digits,
+// K = in_dim * l, k = j l + t - 1) times KSK [K x (n+1)] (u64). Each KSK entry
+// is split into its 8 bytes, KSK = sum_b 2^{8b} P_b with P_b in [0, 255], so
+//     D x KSK = sum_b 2^{8b} (D x P_b)          (mod 2^64)
+// and every D x P_b is an exact int8 x uint8 -> int32 product
+// (|sum| <= K 2^{B-1} 255 < 2^31, checked on the host). The 8 byte planes of
+// 32 output columns form one N = 256 MMA operand, so a CTA owns a 128-row x
+// 32-output tile and recombines the planes in its epilogue.
+//
+// Per CTA (128 ciphertexts x 32 outputs, 256 threads):
+//   * B (byte planes) is pre-arranged once per call (ks_planes_kernel) in the
+//     tensor-core core-matrix layout, so each K-stage is one contiguous bulk
+//     copy (cp.async.bulk, mbarrier completion);
+//   * A (digits) is produced by the threads: each thread decomposes 16 input
+//     coefficients of one ciphertext per stage straight into the core-matrix
+//     layout (no HBM round trip for the digit matrix);
+//   * one thread issues the l MMAs of a stage (M=128, N=256, K=32 each) and
+//     commits them to the stage's "empty" mbarrier; 3 stages in flight;
+//   * the epilogue reads the int32 accumulators from TMEM (thread = ciphertext
+//     row), recombines sum_b C_b << 8b, subtracts from the body column.
+//
+// Shared-memory operand layout (K-major, no swizzle; the canonical UMMA
+// "interleave" layout): 8-row x 16-byte core matrices, core matrix (row group
+// i, 16-byte K chunk kc) at i * SBO + kc * LBO, LBO = 128 B, SBO = 2 l * 128 B.
+#include "common.cuh"
+#include "tmem.cuh"
+
+namespace sz {
+namespace kst {
+
+constexpr int kRows = 128;    // ciphertexts per CTA (MMA M)
+constexpr int kCols = 32;     // output columns per CTA
+constexpr int kN = 8 * kCols;  // MMA N: 8 byte planes x 32 columns
+constexpr int kStages = 3;
+constexpr int kThreads = 256;
+constexpr int kJ = 32;  // input coefficients per K-stage (K_stage = 32 l)
+
+__host__ __device__ constexpr int stage_k(int level) { return kJ * level; }           // bytes of K per stage
+__host__ __device__ constexpr int a_tile(int level) { return kRows * stage_k(level); }  // A bytes per stage
+__host__ __device__ constexpr int b_tile(int level) { return kN * stage_k(level); }     // B bytes per stage
+__host__ __device__ constexpr size_t smem_bytes(int level) {
+  return (size_t)kStages * (a_tile(level) + b_tile(level)) + 8 * (2 * kStages + 1) + 1024;
+}
+// byte offset of (row, k) in a core-matrix tile with K extent kst bytes
+__host__ __device__ constexpr int cm_off(int row, int k, int kst) {
+  return (row >> 3) * (kst / 16) * 128 + (k >> 4) * 128 + (row & 7) * 16 + (k & 15);
+}
+
+// ---------------------------------------------------------- plane preparation
+// planes[cb][stage][b_tile]: row = b * 32 + c (byte b of column 32 cb + c),
+// K index k (within the stage) = row k0 + k of the flat KSK [K][n+1].
+// One thread per (cb, stage, c, 16-byte K chunk): reads 16 u64, writes 8 x 16 bytes.
+__global__ void ks_planes_kernel(const u64 *ksk, unsigned char *planes, int K, int n1, int level, int ncb) {
+  const int kst = stage_k(level), chunks = kst / 16, nst = K / kst;
+  const long total = (long)ncb * nst * kCols * chunks;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    long r = e;
+    const int kc = (int)(r % chunks); r /= chunks;
+    const int c = (int)(r % kCols); r /= kCols;
+    const int st = (int)(r % nst); r /= nst;
+    const int cb = (int)r;
+    const int col = cb * kCols + c;
+    u64 v[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) {
+      const long k = (long)st * kst + kc * 16 + q;
+      v[q] = (col < n1) ? __ldg(&ksk[k * n1 + col]) : 0ull;
+    }
+    unsigned char *tile = planes + ((size_t)cb * nst + st) * b_tile(level);
+#pragma unroll
+    for (int b = 0; b < 8; b++) {
+      uint32_t w[4];
+#pragma unroll
+      for (int q4 = 0; q4 < 4; q4++) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int q = 0; q < 4; q++) x |= (uint32_t)((v[4 * q4 + q] >> (8 * b)) & 0xff) << (8 * q);
+        w[q4] = x;
+      }
+      *reinterpret_cast<uint4 *>(tile + cm_off(b * kCols + c, kc * 16, kst)) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+// --------------------------------------------------------------- primitives
+__device__ __forceinline__ void mbar_init(uint64_t *m, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "SZ_KW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SZ_KW_%=;\n"
+      "}\n" ::"r"(smem_u32(m)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *m) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
+}
+// shared-memory matrix descriptor: K-major, no swizzle (sm_100 descriptor version 1)
+__device__ __forceinline__ uint64_t smem_desc(const void *p, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((smem_u32(p) >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | (1ull << 46);
+}
+// instruction descriptor: D s32, A s8 (signed digits), B u8 (key bytes), K-major both, M = 128, N = 256
+constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (0u << 10) | ((uint32_t)(kN >> 3) << 17) | ((uint32_t)(kRows >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *m) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(m))
+               : "memory");
+}
+
+// ------------------------------------------------------------------ kernel
+struct Args {
+  const u64 *in;                // [count][in_dim+1]
+  const unsigned char *planes;  // [ncb][nst][b_tile]
+  u64 *out;                     // [count][n+1]
+  long count;
+  int in_dim, n1, base_log, level;
+};
+
+template <int L>
+__global__ void __launch_bounds__(kThreads, 1) keyswitch_tc_kernel(Args A) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_slot;
+  unsigned char *smem = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  constexpr int KST = stage_k(L);
+  unsigned char *As = smem;                               // [kStages][a_tile]
+  unsigned char *Bs = smem + kStages * a_tile(L);         // [kStages][b_tile]
+  uint64_t *full = reinterpret_cast<uint64_t *>(Bs + kStages * b_tile(L));
+  uint64_t *empty = full + kStages;
+  uint64_t *done = empty + kStages;
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  // column blocks of one row tile are adjacent in launch order, so the tile's
+  // input rows are fetched from HBM once and re-read from L2
+  const long row0 = (long)blockIdx.y * kRows;
+  const int cb = blockIdx.x;
+  const int nst = A.in_dim * L / KST;
+
+  if (wid == 0) tmem_alloc(&tmem_slot, 256);
+  if (tid == 32) {
+    for (int s = 0; s < kStages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tmem_d = tmem_slot;
+  const unsigned char *Bg = A.planes + (size_t)cb * nst * b_tile(L);
+
+  // producer role of this thread for A: ciphertext row r, half h of the stage's 32 coefficients
+  const int r = tid & (kRows - 1), h = tid >> 7;
+  const long crow = row0 + r;
+  const bool live = crow < A.count;
+  const u64 *arow = A.in + (size_t)(live ? crow : 0) * (A.in_dim + 1);
+
+  if (tid == 0)
+    for (int p = 0; p < kStages - 1 && p < nst; p++) bulk_load(Bs + p * b_tile(L), Bg + (size_t)p * b_tile(L), b_tile(L), &full[p]);
+
+  for (int ks = 0; ks < nst; ks++) {
+    const int s = ks % kStages;
+    // prefetch B of stage ks + kStages - 1 into the buffer MMA ks - 1 is reading
+    const int kp = ks + kStages - 1;
+    if (tid == 0 && kp < nst) {
+      const int sp = kp % kStages;
+      if (kp >= kStages) mbar_wait(&empty[sp], ((kp / kStages) - 1) & 1);
+      bulk_load(Bs + sp * b_tile(L), Bg + (size_t)kp * b_tile(L), b_tile(L), &full[sp]);
+    }
+    // A buffer s was last read by MMA ks - kStages
+    if (ks >= kStages) mbar_wait(&empty[s], ((ks / kStages) - 1) & 1);
+    {
+      // 16 coefficients j = 32 ks + 16 h + jj -> 16 l signed digits, k = jj l + t - 1 (+ 16 h l)
+      uint32_t w[4 * L];  // 16 l bytes
+#pragma unroll
+      for (int q = 0; q < 4 * L; q++) w[q] = 0;
+#pragma unroll
+      for (int jj = 0; jj < 16; jj += 2) {
+        const int j = kJ * ks + 16 * h + jj;
+        const u64 a0 = live ? __ldg(arow + j) : 0ull, a1 = live ? __ldg(arow + j + 1) : 0ull;
+#pragma unroll
+        for (int e = 0; e < 2; e++) {
+          u64 rr = sz_decomp_round(e ? a1 : a0, A.base_log, L);
+#pragma unroll
+          for (int t = L; t >= 1; t--) {
+            const int d = (int)sz_decomp_next(rr, A.base_log);
+            const int k = (jj + e) * L + (t - 1);
+            w[k >> 2] |= (uint32_t)(d & 0xff) << (8 * (k & 3));
+          }
+        }
+      }
+      unsigned char *at = As + s * a_tile(L);
+#pragma unroll
+      for (int c = 0; c < L; c++)
+        *reinterpret_cast<uint4 *>(at + cm_off(r, 16 * (h * L + c), KST)) =
+            make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(&full[s], (ks / kStages) & 1);
+      tmem_fence_after();
+      const unsigned char *at = As + s * a_tile(L);
+      const unsigned char *bt = Bs + s * b_tile(L);
+#pragma unroll
+      for (int q = 0; q < L; q++) {  // K = 32 per MMA: core-matrix chunks 2q, 2q + 1
+        const uint64_t ad = smem_desc(at + q * 256, 128, (KST / 16) * 128);
+        const uint64_t bd = smem_desc(bt + q * 256, 128, (KST / 16) * 128);
+        mma_i8(tmem_d, ad, bd, (ks > 0 || q > 0) ? 1u : 0u);
+      }
+      mma_commit(&empty[s]);
+      if (ks == nst - 1) mma_commit(done);
+    }
+  }
+  // ---- epilogue: thread (warp w, lane) owns ciphertext row 32 (w % 4) + lane,
+  // output columns 16 (w / 4) .. + 15 of this CTA's 32
+  mbar_wait(done, 0);
+  tmem_fence_after();
+  const int er = 32 * (wid & 3) + lane, half = wid >> 2;
+  const long ecrow = row0 + er;
+  u64 acc[16];
+#pragma unroll
+  for (int c = 0; c < 16; c++) acc[c] = 0;
+#pragma unroll
+  for (int b = 0; b < 8; b++) {
+    uint32_t v[16];
+    tmem_ld16(tmem_d + ((uint32_t)(32 * (wid & 3)) << 16) + b * kCols + 16 * half, v);
+    tmem_wait_ld16(v);
+#pragma unroll
+    for (int c = 0; c < 16; c++) acc[c] += (u64)(i64)(int32_t)v[c] << (8 * b);
+  }
+  if (ecrow < A.count) {
+    const u64 *irow = A.in + (size_t)ecrow * (A.in_dim + 1);
+    u64 *orow = A.out + (size_t)ecrow * A.n1;
+#pragma unroll
+    for (int c = 0; c < 16; c++) {
+      const int col = cb * kCols + 16 * half + c;
+      if (col < A.n1) orow[col] = ((col == A.n1 - 1) ? irow[A.in_dim] : 0ull) - acc[c];
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (wid == 0) tmem_dealloc(tmem_slot, 256);
+}
+
+}  // namespace kst
+
+// ------------------------------------------------------------------ host side
+static bool ks_tc_applicable(int in_dim, int level, int base_log) {
+  if (level < 1 || level > 8 || base_log < 1 || base_log > 7) return false;  // digits must fit int8
+  if (in_dim % kst::kJ) return false;
+  const double bound = (double)in_dim * level * (double)(1 << (base_log - 1)) * 255.0;
+  if (bound >= 2147483648.0) return false;  // int32 accumulation must stay exact
+  return kst::smem_bytes(level) <= 227 * 1024;
+}
+
+size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log) {
+  if (!ks_tc_applicable(in_dim, level, base_log)) return 0;
+  const size_t ncb = (size_t)(n + 1 + kst::kCols - 1) / kst::kCols;
+  return ncb * (size_t)in_dim * level * kst::kN;
+}
+
+int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, int in_dim, int n, int base_log,
+                        int level, void *workspace, cudaStream_t stream) {
+  if (!ks_tc_applicable(in_dim, level, base_log)) return SILENZIO_ERR_UNSUPPORTED;
+  if (((uintptr_t)workspace & 15) != 0) return SILENZIO_ERR_MISALIGNED;
+  const int n1 = n + 1, K = in_dim * level;
+  const int ncb = (n1 + kst::kCols - 1) / kst::kCols;
+  unsigned char *planes = reinterpret_cast<unsigned char *>(workspace);
+  {
+    const long total = (long)ncb * (K / kst::stage_k(level)) * kst::kCols * (kst::stage_k(level) / 16);
+    const int threads = 256;
+    const long blocks = (total + threads - 1) / threads;
+    kst::ks_planes_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, stream>>>(ksk, planes, K, n1, level, ncb);
+    SZ_LAUNCH_OK();
+  }
+  void (*kern)(kst::Args) = nullptr;
+  switch (level) {
+    case 1: kern = kst::keyswitch_tc_kernel<1>; break;
+    case 2: kern = kst::keyswitch_tc_kernel<2>; break;
+    case 3: kern = kst::keyswitch_tc_kernel<3>; break;
+    case 4: kern = kst::keyswitch_tc_kernel<4>; break;
+    case 5: kern = kst::keyswitch_tc_kernel<5>; break;
+    case 6: kern = kst::keyswitch_tc_kernel<6>; break;
+    default: return SILENZIO_ERR_UNSUPPORTED;
+  }
+  const size_t smem = kst::smem_bytes(level);
+  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t max_rows = (size_t)65535 * kst::kRows;  // grid.y limit per launch
+  for (size_t c0 = 0; c0 < count; c0 += max_rows) {
+    const size_t cnt = count - c0 < max_rows ? count - c0 : max_rows;
+    kst::Args A{in + c0 * (size_t)(in_dim + 1), planes, out + c0 * (size_t)n1, (long)cnt, in_dim, n1, base_log, level};
+    dim3 grid((unsigned)ncb, (unsigned)((cnt + kst::kRows - 1) / kst::kRows));
+    kern<<<grid, kst::kThreads, smem, stream>>>(A);
+    SZ_LAUNCH_OK();
+  }
+  return SILENZIO_OK;
+}
+
+}  // namespace sz

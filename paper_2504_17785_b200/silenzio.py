@@ -45,7 +45,8 @@ def load():
         "silenzio_pbs_host_workspace_bytes": ([P, S], S),
         "silenzio_pbs_launch_count": ([P, S], ctypes.c_long),
         "silenzio_bsk_to_fourier": ([V, V, P, V], I),
-        "silenzio_keyswitch_batch": ([V, V, V, S, P, V], I),
+        "silenzio_keyswitch_batch": ([V, V, V, S, P, V, V], I),
+        "silenzio_keyswitch_workspace_bytes": ([P, S], S),
         "silenzio_pbs_batch": ([V, V, V, U32, V, V, V, S, P, V, V], I),
         "silenzio_blind_rotate_batch": ([V, V, V, U32, V, V, S, P, V, V], I),
         "silenzio_blind_rotate_workspace_bytes": ([P, S], S),
@@ -79,7 +80,7 @@ def exported_symbols():
     return [
         "silenzio_status_string", "silenzio_version", "silenzio_fourier_bsk_bytes",
         "silenzio_pbs_workspace_bytes", "silenzio_pbs_host_workspace_bytes", "silenzio_pbs_launch_count",
-        "silenzio_bsk_to_fourier", "silenzio_keyswitch_batch", "silenzio_pbs_batch",
+        "silenzio_bsk_to_fourier", "silenzio_keyswitch_batch", "silenzio_keyswitch_workspace_bytes", "silenzio_pbs_batch",
         "silenzio_blind_rotate_batch", "silenzio_blind_rotate_workspace_bytes", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
         "silenzio_build_testpoly", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
         "silenzio_bsk_generate", "silenzio_bsk_generate_workspace_bytes", "silenzio_ksk_generate", "silenzio_rns_matmul_workspace_bytes",
@@ -164,12 +165,22 @@ def bsk_to_fourier(bsk, P, stream=None):
     return out
 
 
-def keyswitch_batch(lwe_in, ksk, P, out=None, stream=None):
+def keyswitch_workspace_bytes(P, count: int = 0) -> int:
+    return load().silenzio_keyswitch_workspace_bytes(ctypes.byref(make_params(P)), count)
+
+
+def keyswitch_batch(lwe_in, ksk, P, out=None, stream=None, tensor_cores=True, workspace=None):
+    """Keyswitch; tensor_cores=True gives the library a workspace so it can use the
+    tcgen05 int8 path (when the parameters admit it), False forces the CUDA-core kernel."""
     count = lwe_in.shape[0]
     if out is None:
         out = torch.empty((count, P.n + 1), dtype=torch.int64, device=lwe_in.device)
+    if workspace is None and tensor_cores:
+        nbytes = keyswitch_workspace_bytes(P, count)
+        if nbytes:
+            workspace = torch.empty(nbytes, dtype=torch.uint8, device=lwe_in.device)
     _check(load().silenzio_keyswitch_batch(_ptr(lwe_in), _ptr(ksk), _ptr(out), count,
-                                           ctypes.byref(make_params(P)), _stream(stream)))
+                                           ctypes.byref(make_params(P)), _ptr(workspace), _stream(stream)))
     return out
 
 

@@ -69,16 +69,46 @@ def test_testpoly_bitexact(dev):
 
 
 # --------------------------------------------------------------- keyswitch
-@pytest.mark.parametrize("cnt", [1, 37, 256])
-def test_keyswitch_bitexact(cnt, dev):
+@pytest.mark.parametrize("tensor_cores", [True, False])
+@pytest.mark.parametrize("cnt", [1, 37, 256, 300])
+def test_keyswitch_bitexact(cnt, tensor_cores, dev):
+    """Both keyswitch kernels (tcgen05 int8 byte-plane GEMM, CUDA-core) equal
+    the oracle bit for bit; 300 = two full 128-row tiles + a ragged one, and
+    n + 1 = 743 leaves a ragged 32-column block."""
     from paper_2504_17785_b200 import silenzio, workload as wl
     P, rnd, ok, gk = _setup("A", 4, dev)
+    if tensor_cores:
+        assert silenzio.keyswitch_workspace_bytes(P) > 0
     r = lwe_randomness(P, cnt, 4)
     m = messages(cnt, P.p, 4)
     ct = oracle.lwe_encrypt(oracle.encode(m, P.p), ok["big_key"], r["mask"], r["noise"])
-    out_g = u64(silenzio.keyswitch_batch(wl.to_dev(ct, dev), gk["ksk"], P))
+    out_g = u64(silenzio.keyswitch_batch(wl.to_dev(ct, dev), gk["ksk"], P, tensor_cores=tensor_cores))
     out_o = oracle.keyswitch(ct, ok["ksk"], P)
     assert np.array_equal(out_g, out_o)
+
+
+def test_keyswitch_tensor_core_extremes(dev):
+    """Digit and byte extremes: coefficients at 0, 2^63, 2^64-1 and at the
+    rounding boundaries of the 15-bit decomposition (carry chains through all
+    five digits, d = -4 everywhere), KSK rows of all-ones bytes (the largest
+    int32 partial sums) and zeros."""
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P = get_params("A")
+    rng = np.random.default_rng(11)
+    in_dim, L = P.big_dim, P.ks_level
+    ksk = rng.integers(0, 2 ** 64, size=(in_dim, L, P.n + 1), dtype=np.uint64)
+    ksk[: in_dim // 2, :, ::3] = np.uint64(2 ** 64 - 1)
+    ksk[in_dim // 2:, :, 1::5] = np.uint64(0)
+    half = 1 << (64 - 15 - 1)
+    specials = np.array([0, 2 ** 63, 2 ** 64 - 1, half, half - 1, 2 ** 64 - half, 2 ** 64 - half - 1,
+                         (2 ** 64 - 1) ^ ((1 << 49) - 1)], dtype=np.uint64)
+    cnt = 130
+    ct = rng.integers(0, 2 ** 64, size=(cnt, in_dim + 1), dtype=np.uint64)
+    for i, v in enumerate(specials):
+        ct[i, :] = v
+    ct[len(specials):len(specials) + 4, :in_dim] = specials[rng.integers(0, len(specials), size=(4, in_dim))]
+    out_g = u64(silenzio.keyswitch_batch(wl.to_dev(ct, dev), wl.to_dev(ksk, dev), P, tensor_cores=True))
+    assert np.array_equal(out_g, oracle.keyswitch(ct, ksk, P))
 
 
 # --------------------------------------------------------------------- PBS
