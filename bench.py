@@ -205,11 +205,13 @@ def main():
     small = torch.empty((B, P.n + 1), dtype=torch.int64, device=dev)
     out = torch.empty((B, P.big_dim + 1), dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
+    # keyswitch workspace: the KSK byte planes of the tensor-core keyswitch (re-derived every step)
+    ks_ws = torch.empty(max(silenzio.keyswitch_workspace_bytes(P, B), 16), dtype=torch.uint8, device=dev)
 
     def step(ev=None):
         if ev is not None:
             ev[0].record(stream)
-        silenzio.keyswitch_batch(ct, keys["ksk"], P, out=small, stream=stream)
+        silenzio.keyswitch_batch(ct, keys["ksk"], P, out=small, stream=stream, workspace=ks_ws)
         if ev is not None:
             ev[1].record(stream)
         silenzio.blind_rotate_batch(small, ids, luts, keys["fbsk"], P, out=out, stream=stream)
@@ -278,14 +280,19 @@ def main():
         return
 
     flops = pbs_flops(P)
+    ks_ops = 2.0 * P.big_dim * P.ks_level * (P.n + 1) * 8  # 8 byte-plane int8 GEMM MACs per ciphertext
     launches = int(args.steps * silenzio.pbs_launch_count(P, B))
     br_avg_s = float(np.mean(br_ms)) / 1e3
     achieved = flops * B / br_avg_s / 1e12
     roofline = {"bound": "alu", "pipe": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                "kernel": "blind_rotate_kernel", "algorithmic_flops_per_pbs": flops,
+                "kernel": "blind_rotate_warp_kernel<3>", "algorithmic_flops_per_pbs": flops,
                 "kernel_ms": float(np.mean(br_ms)), "keyswitch_ms": float(np.mean(ks_ms)),
-                "peak_source": "measured DFMA burst (tools/microbench/mb.cu, profiles/fp64_peak.txt)",
+                "peak_source": "measured DFMA burst (tools/microbench/mb.cu, profiles/r01_microbench_b200.txt)",
+                "keyswitch": {"kernel": "keyswitch_tc_kernel<5> (tcgen05 kind::i8)",
+                              "int8_tensor_tops": ks_ops * B / (float(np.mean(ks_ms)) / 1e3) / 1e12,
+                              "peak_int8_tops_nominal": 4500.0,
+                              "ops_per_ct": ks_ops},
                 "pbs_roofline_pbs_per_s": FP64_PEAK_TFLOPS * 1e12 / flops,
                 "frac_of_pbs_roofline_whole_step": value / world / (FP64_PEAK_TFLOPS * 1e12 / flops)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

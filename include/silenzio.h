@@ -74,8 +74,10 @@ size_t silenzio_fourier_bsk_bytes(const silenzio_params *params);
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *params, size_t count);
 
 /* Number of kernel launches silenzio_pbs_batch makes for `count` ciphertexts:
- * one keyswitch plus one blind rotation per resident wave (all CTAs of a wave
- * sweep the Fourier BSK together). -1 if the parameters are unsupported. */
+ * the keyswitch (tensor-core path: KSK byte-plane preparation + one GEMM per
+ * 65535 x 128 ciphertexts; CUDA-core path: one) plus one blind rotation per
+ * resident wave (all CTAs of a wave sweep the Fourier BSK together).
+ * -1 if the parameters are unsupported. */
 long silenzio_pbs_launch_count(const silenzio_params *params, size_t count);
 
 /* ------------------------------------------------------- hot-path calls */

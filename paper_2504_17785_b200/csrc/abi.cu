@@ -211,7 +211,9 @@ long silenzio_pbs_launch_count(const silenzio_params *P, size_t count) {
                    : P->poly_size == 32768 ? blind_rotate_huge_wave(P)
                                            : blind_rotate_wave(P);
   if (wave <= 0) return -1;
-  return 1 + (long)((count + wave - 1) / wave);  // keyswitch + one blind rotation per wave
+  // keyswitch: byte-plane preparation + one GEMM launch per 65535 row tiles (tensor cores), else one launch
+  const long ks = silenzio_keyswitch_workspace_bytes(P, count) > 0 ? 1 + (long)((count + 65535L * 128 - 1) / (65535L * 128)) : 1;
+  return ks + (long)((count + wave - 1) / wave);  // + one blind rotation per wave
 }
 
 size_t silenzio_pbs_host_workspace_bytes(const silenzio_params *P, size_t chunk) {

@@ -182,7 +182,16 @@ __global__ void __launch_bounds__(kThreads, 1) keyswitch_tc_kernel(Args A) {
   if (tid == 0)
     for (int p = 0; p < kStages - 1 && p < nst; p++) bulk_load(Bs + p * b_tile(L), Bg + (size_t)p * b_tile(L), b_tile(L), &full[p]);
 
+  // this thread's 16 input coefficients of the current stage; the next stage's
+  // are loaded one iteration ahead so their latency hides behind this stage
+  u64 av[16];
+#pragma unroll
+  for (int q = 0; q < 16; q++) av[q] = live ? __ldg(arow + 16 * h + q) : 0ull;
+
   for (int ks = 0; ks < nst; ks++) {
+    u64 nx[16];
+#pragma unroll
+    for (int q = 0; q < 16; q++) nx[q] = (live && ks + 1 < nst) ? __ldg(arow + kJ * (ks + 1) + 16 * h + q) : 0ull;
     const int s = ks % kStages;
     // prefetch B of stage ks + kStages - 1 into the buffer MMA ks - 1 is reading
     const int kp = ks + kStages - 1;
@@ -199,18 +208,13 @@ __global__ void __launch_bounds__(kThreads, 1) keyswitch_tc_kernel(Args A) {
 #pragma unroll
       for (int q = 0; q < 4 * L; q++) w[q] = 0;
 #pragma unroll
-      for (int jj = 0; jj < 16; jj += 2) {
-        const int j = kJ * ks + 16 * h + jj;
-        const u64 a0 = live ? __ldg(arow + j) : 0ull, a1 = live ? __ldg(arow + j + 1) : 0ull;
+      for (int jj = 0; jj < 16; jj++) {
+        u64 rr = sz_decomp_round(av[jj], A.base_log, L);
 #pragma unroll
-        for (int e = 0; e < 2; e++) {
-          u64 rr = sz_decomp_round(e ? a1 : a0, A.base_log, L);
-#pragma unroll
-          for (int t = L; t >= 1; t--) {
-            const int d = (int)sz_decomp_next(rr, A.base_log);
-            const int k = (jj + e) * L + (t - 1);
-            w[k >> 2] |= (uint32_t)(d & 0xff) << (8 * (k & 3));
-          }
+        for (int t = L; t >= 1; t--) {
+          const int d = (int)sz_decomp_next(rr, A.base_log);
+          const int k = jj * L + (t - 1);
+          w[k >> 2] |= (uint32_t)(d & 0xff) << (8 * (k & 3));
         }
       }
       unsigned char *at = As + s * a_tile(L);
@@ -235,6 +239,8 @@ __global__ void __launch_bounds__(kThreads, 1) keyswitch_tc_kernel(Args A) {
       mma_commit(&empty[s]);
       if (ks == nst - 1) mma_commit(done);
     }
+#pragma unroll
+    for (int q = 0; q < 16; q++) av[q] = nx[q];
   }
   // ---- epilogue: thread (warp w, lane) owns ciphertext row 32 (w % 4) + lane,
   // output columns 16 (w / 4) .. + 15 of this CTA's 32

@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k keyswitch > gpurun_out/diag14.txt 2>&1
-timeout 600 python tools/kst_bench.py >> gpurun_out/diag14.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k keyswitch > gpurun_out/diag15.txt 2>&1
+timeout 600 python tools/kst_bench.py >> gpurun_out/diag15.txt 2>&1
