@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k keyswitch > gpurun_out/diag15.txt 2>&1
-timeout 600 python tools/kst_bench.py >> gpurun_out/diag15.txt 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke3.log 2>&1; echo smoke rc=$? >> gpurun_out/smoke3.log
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_all2.log 2>&1; echo rc=$? >> gpurun_out/gpu_all2.log
