@@ -22,7 +22,7 @@
 //    during the inverse FFT (mbarrier completion).
 //
 // Fourier BSK layout for this kernel: [n][P][2 (o)][2 (row)][32 (r)][32 (lane)]
-// where (r, lane) holds the spectrum at index lane + 32 bitrev5(r), times 1/M.
+// where (r, lane) holds the spectrum at index lane + 32 r, times 1/M.
 #include <cmath>
 #include <mutex>
 
@@ -83,10 +83,28 @@ __device__ __forceinline__ double2 mulw32v(double2 d, int e) {
   }
 }
 
-// In-place radix-2 DIF DFT of size 32 on registers, exponent sign + (conjugate
-// when INV). Natural-order input, bit-reversed output: x[r] = X[bitrev5(r)].
+// Variant switches. All 32 combinations were built (tools/build_warp_variants.sh)
+// and timed on a B200 (profiles/r01_warp_variants.txt): the spread is 31-39 k
+// PBS/s from register allocation alone; the defaults are the fastest.
+#ifndef SZ_DFT_DIT
+#define SZ_DFT_DIT 1  // DIT with 6-op FMA butterflies (9 % fewer FP64 ops than DIF)
+#endif
+#ifndef SZ_TW_SMEM
+#define SZ_TW_SMEM 1  // four-step twiddles staged in shared memory (one swizzled table)
+#endif
+#ifndef SZ_ACC_FAST
+#define SZ_ACC_FAST 0  // limb recombination without per-limb offset correction
+#endif
+#ifndef SZ_INV_TW_POST
+#define SZ_INV_TW_POST 1  // inverse untwiddle after the transposition
+#endif
+#ifndef SZ_MAC_X32
+#define SZ_MAC_X32 1  // 32-column TMEM loads of the digit spectra in the MAC
+#endif
+
+// Radix-2 decimation-in-frequency stages (natural in, bit-reversed out), half size H = 16..1
 template <bool INV, int H>
-__device__ __forceinline__ void dft32_stage(double2 (&x)[32]) {
+__device__ __forceinline__ void dif32_stage(double2 (&x)[32]) {
   if constexpr (H >= 1) {
 #pragma unroll
     for (int b = 0; b < 32; b += 2 * H)
@@ -96,28 +114,120 @@ __device__ __forceinline__ void dft32_stage(double2 (&x)[32]) {
         x[b + j] = cadd(a, c);
         x[b + j + H] = mulw32v<INV>(csub(a, c), j * (16 / H));  // W_{2H}^j = W_32^{j 32/(2H)}
       }
-    dft32_stage<INV, H / 2>(x);
+    dif32_stage<INV, H / 2>(x);
+  }
+}
+
+// tan(2 pi r / 32), r = 0..4 (correctly rounded doubles)
+struct T32 {
+  static constexpr double t[5] = {0.0, 0.198912367379658, 0.41421356237309503, 0.6681786379192989, 1.0};
+};
+
+// DIT butterfly a' = a + W^E b, b' = a - W^E b, W = e^{+2 pi i / 32} (conjugate
+// when INV), 6 FP64 instructions when nontrivial: with W^e = i^q e^{i theta},
+//   e^{i theta} b = cos (b.x - tan b.y, b.y + tan b.x) = sin (cot b.x - b.y, cot b.y + b.x)
+// and the cos / sin scale folds into the four output FMAs.
+template <int E, bool INV>
+__device__ __forceinline__ void bfly(double2 &a, double2 &b) {
+  constexpr int e = INV ? ((32 - (E & 31)) & 31) : (E & 31);
+  constexpr int q = e >> 3, r = e & 7;
+  if constexpr (r == 0) {
+    double2 t;
+    if constexpr (q == 0) t = b;
+    else if constexpr (q == 1) t = make_double2(-b.y, b.x);
+    else if constexpr (q == 2) t = make_double2(-b.x, -b.y);
+    else t = make_double2(b.y, -b.x);
+    const double2 na = cadd(a, t), nb = csub(a, t);
+    a = na;
+    b = nb;
+  } else {
+    double u, v;
+    if constexpr (r <= 4) {
+      constexpr double tn = T32::t[r];
+      u = fma(-tn, b.y, b.x);
+      v = fma(tn, b.x, b.y);
+    } else {
+      constexpr double ct = T32::t[8 - r];
+      u = fma(ct, b.x, -b.y);
+      v = fma(ct, b.y, b.x);
+    }
+    constexpr double f = (r <= 4) ? C32::c[r] : C32::c[8 - r];
+    double U, V;  // (u + i v) * i^q
+    if constexpr (q == 0) { U = u; V = v; }
+    else if constexpr (q == 1) { U = -v; V = u; }
+    else if constexpr (q == 2) { U = -u; V = -v; }
+    else { U = v; V = -u; }
+    const double2 na = make_double2(fma(f, U, a.x), fma(f, V, a.y));
+    const double2 nb = make_double2(fma(-f, U, a.x), fma(-f, V, a.y));
+    a = na;
+    b = nb;
   }
 }
 template <bool INV>
-__device__ __forceinline__ void dft32(double2 (&x)[32]) {
-  dft32_stage<INV, 16>(x);
+__device__ __forceinline__ void bfly_v(double2 &a, double2 &b, int e) {
+  switch (e & 31) {
+#define SZ_B(k) \
+  case k: bfly<k, INV>(a, b); break;
+    SZ_B(0) SZ_B(1) SZ_B(2) SZ_B(3) SZ_B(4) SZ_B(5) SZ_B(6) SZ_B(7)
+    SZ_B(8) SZ_B(9) SZ_B(10) SZ_B(11) SZ_B(12) SZ_B(13) SZ_B(14) SZ_B(15)
+#undef SZ_B
+    default: break;
+  }
+}
+// Radix-2 decimation-in-time stages on the bit-reversed view, half size H = 1..16
+template <bool INV, int H>
+__device__ __forceinline__ void dit32_stage(double2 (&y)[32]) {
+  if constexpr (H <= 16) {
+#pragma unroll
+    for (int b = 0; b < 32; b += 2 * H)
+#pragma unroll
+      for (int j = 0; j < H; j++) bfly_v<INV>(y[b + j], y[b + j + H], j * (16 / H));
+    dit32_stage<INV, 2 * H>(y);
+  }
 }
 
 __host__ __device__ constexpr int bitrev5(int r) {
   return ((r & 1) << 4) | ((r & 2) << 2) | (r & 4) | ((r & 8) >> 2) | ((r & 16) >> 4);
 }
 
+// 32-point DFT on registers, exponent sign + (conjugate when INV), natural-order
+// input and output: X[k] = sum_n x[n] e^{+-2 pi i n k / 32}; the bit reversal
+// of either radix-2 form is a register renaming.
+template <bool INV>
+__device__ __forceinline__ void dft32(double2 (&x)[32]) {
+  double2 y[32];
+#if SZ_DFT_DIT
+#pragma unroll
+  for (int r = 0; r < 32; r++) y[r] = x[bitrev5(r)];
+  dit32_stage<INV, 1>(y);
+#pragma unroll
+  for (int r = 0; r < 32; r++) x[r] = y[r];
+#else
+#pragma unroll
+  for (int r = 0; r < 32; r++) y[r] = x[r];
+  dif32_stage<INV, 16>(y);
+#pragma unroll
+  for (int r = 0; r < 32; r++) x[bitrev5(r)] = y[r];
+#endif
+}
+
 // Tables (host-built in long double, rounded once), w = e^{i pi / 2048}:
-//   tw [k1 * 32 + l] = w^{l (1 + 4 k1)}  (negacyclic twist w^l folded with the
-//   twT[l * 32 + k1] = same value         four-step twiddle e^{2 pi i l k1 / M})
-//   c_twist32[m]     = w^{32 m} = e^{i pi m / 64}
+//   T(l, k1)     = w^{l (1 + 4 k1)}  (negacyclic twist w^l folded with the
+//                  four-step twiddle e^{2 pi i l k1 / M}), stored as
+//   tw [k1 * 32 + l], twT[l * 32 + k1] (coalesced for lane = l / lane = k1) and
+//   tws[sw(l, k1)]  (swizzled, for the shared-memory copy: conflict free both ways)
+//   c_twist32[m]  = w^{32 m} = e^{i pi m / 64}
 struct Tables32 {
   double2 tw[32 * 32];
   double2 twT[32 * 32];
+  double2 tws[32 * 32];
 };
 __device__ Tables32 g_t32;
 __constant__ double2 c_twist32[32];
+
+// swizzled index of element (row, col) of a 32 x 32 block of 16-byte values:
+// any 8 consecutive rows (fixed col) or cols (fixed row) hit 8 distinct 16-byte bank groups
+__host__ __device__ constexpr int sw(int row, int col) { return row * 32 + (col ^ (row & 7)); }
 
 static std::once_flag g_once[64];
 static int g_status[64];
@@ -132,6 +242,7 @@ static int init_tables(int dev) {
       const double2 v = make_double2((double)cosl(ang), (double)sinl(ang));
       h.tw[k1 * 32 + l] = v;
       h.twT[l * 32 + k1] = v;
+      h.tws[sw(l, k1)] = v;
     }
   for (int m = 0; m < 32; m++) {
     const long double ang = PI * (long double)m / 64.0L;
@@ -153,49 +264,59 @@ static int ensure_tables() {
   return g_status[dev];
 }
 
-// swizzled index of element (row, col) of a 32 x 32 block of 16-byte values:
-// any 8 consecutive rows (fixed col) or cols (fixed row) hit 8 distinct 16-byte bank groups
-__device__ __forceinline__ int sw(int row, int col) { return row * 32 + (col ^ (row & 7)); }
+// twiddle T(l, k1): from the shared-memory copy (`sm`) or the global tables
+__device__ __forceinline__ double2 tw_fwd(const double2 *sm, int l, int k1) {  // lane = l
+#if SZ_TW_SMEM
+  return sm[sw(l, k1)];
+#else
+  (void)sm;
+  return __ldg(&g_t32.tw[k1 * 32 + l]);
+#endif
+}
+__device__ __forceinline__ double2 tw_inv(const double2 *sm, int l, int k1) {  // lane = k1
+#if SZ_TW_SMEM
+  return sm[sw(l, k1)];
+#else
+  (void)sm;
+  return __ldg(&g_t32.twT[l * 32 + k1]);
+#endif
+}
 
 // Forward transform of one warp. In: x[m] = (a_j + i a_{j+1024}) at j = lane + 32 m.
-// Out: x[r] = spectrum at index lane + 32 bitrev5(r) ("slot" order).
-__device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, int lane) {
+// Out: x[k2] = spectrum at index lane + 32 k2 ("slot" order). `tsm` = shared twiddle copy (SZ_TW_SMEM).
+__device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, const double2 *tsm, int lane) {
 #pragma unroll
   for (int m = 1; m < 32; m++) x[m] = cmul(x[m], c_twist32[m]);
-  dft32<false>(x);  // x[r] = B[l = lane][k1 = bitrev5(r)]
+  dft32<false>(x);  // x[k1] = B[l = lane][k1]
   __syncwarp();     // earlier readers of buf are done
 #pragma unroll
-  for (int r = 0; r < 32; r++) {
-    const int k1 = bitrev5(r);
-    buf[sw(lane, k1)] = cmul(x[r], __ldg(&g_t32.tw[k1 * 32 + lane]));
-  }
+  for (int k1 = 0; k1 < 32; k1++) buf[sw(lane, k1)] = cmul(x[k1], tw_fwd(tsm, lane, k1));
   __syncwarp();
 #pragma unroll
   for (int l = 0; l < 32; l++) x[l] = buf[sw(l, lane)];  // thread k1 = lane, natural l
-  dft32<false>(x);
+  dft32<false>(x);                                        // x[k2] = Z[lane + 32 k2]
 }
 
 // Inverse transform (unnormalised). In: slot order. Out: x[m] = M (c_j + i c_{j+1024}), j = lane + 32 m.
-__device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, int lane) {
-  double2 z[32];
+__device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, const double2 *tsm, int lane) {
+  dft32<true>(x);  // x[l] = 32 B'[l][k1 = lane]
+  __syncwarp();
+#if SZ_INV_TW_POST
 #pragma unroll
-  for (int r = 0; r < 32; r++) z[bitrev5(r)] = x[r];  // natural k2
-  dft32<true>(z);                                     // z[r] = 32 B'[l = bitrev5(r)][k1 = lane]
+  for (int l = 0; l < 32; l++) buf[sw(l, lane)] = x[l];
   __syncwarp();
 #pragma unroll
-  for (int r = 0; r < 32; r++) {
-    const int l = bitrev5(r);
-    buf[sw(l, lane)] = cmulc(z[r], __ldg(&g_t32.twT[l * 32 + lane]));
-  }
+  for (int k1 = 0; k1 < 32; k1++) x[k1] = cmulc(buf[sw(lane, k1)], tw_fwd(tsm, lane, k1));  // thread l = lane
+#else
+#pragma unroll
+  for (int l = 0; l < 32; l++) buf[sw(l, lane)] = cmulc(x[l], tw_inv(tsm, l, lane));
   __syncwarp();
 #pragma unroll
-  for (int k1 = 0; k1 < 32; k1++) z[k1] = buf[sw(lane, k1)];  // thread l = lane, natural k1
-  dft32<true>(z);                                             // z[r] = M z_{lane + 32 m} w^{32 m}, m = bitrev5(r)
+  for (int k1 = 0; k1 < 32; k1++) x[k1] = buf[sw(lane, k1)];  // thread l = lane, natural k1
+#endif
+  dft32<true>(x);  // x[m] = M z_{lane + 32 m} w^{32 m}
 #pragma unroll
-  for (int r = 0; r < 32; r++) {
-    const int m = bitrev5(r);
-    x[m] = (m == 0) ? z[r] : cmulc(z[r], c_twist32[m]);
-  }
+  for (int m = 1; m < 32; m++) x[m] = cmulc(x[m], c_twist32[m]);
 }
 
 // ------------------------------------------------------------ mbarrier / bulk copy
@@ -240,6 +361,7 @@ __host__ __device__ constexpr size_t abar_bytes(int n) { return ((size_t)n * 2 +
 __host__ __device__ constexpr size_t smem_bytes(int n) {
   return 8 * (size_t)kM * sizeof(double2)    // per-warp transposition buffers (also the ACC copy)
          + 4 * (size_t)kM * sizeof(double2)  // BSK stage: one (i, limb), [o][row][32][32]
+         + (SZ_TW_SMEM ? (size_t)kM * sizeof(double2) : 0)  // twiddle table copy
          + kCts * abar_bytes(n)              // modswitched masks
          + 16;                               // mbarrier
 }
@@ -271,6 +393,11 @@ __device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[4][2]
   tmem_st16(ta + 16 * cc, r);
 }
 
+// bits of x + 1.5 * 2^52: round(x) + bits(1.5 * 2^52) for |x| < 2^51 (see rint_small)
+__device__ __forceinline__ u64 limb_bits(double x) { return (u64)__double_as_longlong(x + 6755399441055744.0); }
+constexpr u64 kMagicBits = 0x4338000000000000ull;  // bits of 1.5 * 2^52
+constexpr u64 kLimbOffset3 = kMagicBits + (kMagicBits << 22) + (kMagicBits << 44);  // sum_p bits(M) << 22 p
+
 template <int P>
 __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -278,7 +405,8 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   const int n = A.n, w = A.w, blog = A.base_log;
   double2 *xbuf_all = reinterpret_cast<double2 *>(smem);
   double2 *gbuf = xbuf_all + 8 * kM;
-  unsigned char *abar_base = reinterpret_cast<unsigned char *>(gbuf + 4 * kM);
+  double2 *tsm = gbuf + 4 * kM;  // twiddle copy (SZ_TW_SMEM)
+  unsigned char *abar_base = reinterpret_cast<unsigned char *>(tsm + (SZ_TW_SMEM ? kM : 0));
   uint64_t *mbar = reinterpret_cast<uint64_t *>(abar_base + kCts * abar_bytes(n));
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int cs = wid & 3, g = wid >> 2;  // ciphertext slot, GLWE component
@@ -288,6 +416,9 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
 
   if (wid == 0) tmem_alloc(&tmem_slot, kTmemCols);
   if (tid == 32) mbar_init(mbar, 1);
+#if SZ_TW_SMEM
+  for (int e = tid; e < kM; e += kThreads) tsm[e] = g_t32.tws[e];
+#endif
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -365,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
           x[4 * cc + q] = make_double2(dv[0], dv[1]);
         }
       }
-      fwd_fft32(x, xbuf, lane);
+      fwd_fft32(x, xbuf, tsm, lane);
       if (i > 0) {  // both warps of the ciphertext are past the previous CMux's MACs (D^ reads)
         tmem_fence_before();
         asm volatile("bar.sync %0, %1;" ::"r"(5 + cs), "r"(64) : "memory");
@@ -389,6 +520,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
         double2 y[32];
         const double2 *G0 = gbuf + (size_t)(2 * g) * kM + lane;  // [o = g][row 0]
         const double2 *G1 = G0 + kM;                             // [o = g][row 1]
+#if SZ_MAC_X32
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) {
           uint32_t d0[32], d1[32];
@@ -404,6 +536,23 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
             y[r] = acc;
           }
         }
+#else
+#pragma unroll
+        for (int jj = 0; jj < 8; jj++) {
+          uint32_t d0[16], d1[16];
+          tmem_ld16(ta_d0 + 16 * jj, d0);
+          tmem_ld16(ta_d1 + 16 * jj, d1);
+          tmem_wait_ld16x2(d0, d1);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int r = 4 * jj + q;
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, unpack1(d0, q), G0[r * 32]);
+            cmac(acc, unpack1(d1, q), G1[r * 32]);
+            y[r] = acc;
+          }
+        }
+#endif
         // this warp is done with the stage; the last of the 8 warps re-arms it
         // with the next (i, limb) -- no CTA-wide barrier
         __syncwarp();
@@ -414,14 +563,27 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
             else if (i + 1 < n) issue(i + 1, P - 1);
           }
         }
-        inv_fft32(y, xbuf, lane);
+        inv_fft32(y, xbuf, tsm, lane);
 #pragma unroll
         for (int cc = 0; cc < 8; cc++) {
           u64 a4[4][2];
           acc_ld(ta_acc, cc, a4);
 #pragma unroll
           for (int q = 0; q < 4; q++) {
-            if (P == 3) {
+            if (SZ_ACC_FAST && P == 3 && w == 22) {
+              // round(x) << 22p via the 1.5 * 2^52 trick; the magic constant's
+              // bits are removed once per CMux (kLimbOffset3, at p = 0)
+              if (p == 2) {
+                a4[q][0] += (u64)((uint32_t)limb_bits(y[4 * cc + q].x) << 12) << 32;
+                a4[q][1] += (u64)((uint32_t)limb_bits(y[4 * cc + q].y) << 12) << 32;
+              } else if (p == 1) {
+                a4[q][0] += limb_bits(y[4 * cc + q].x) << 22;
+                a4[q][1] += limb_bits(y[4 * cc + q].y) << 22;
+              } else {
+                a4[q][0] += limb_bits(y[4 * cc + q].x) - kLimbOffset3;
+                a4[q][1] += limb_bits(y[4 * cc + q].y) - kLimbOffset3;
+              }
+            } else if (P == 3) {
               a4[q][0] += rint_small(y[4 * cc + q].x) << (p * w);
               a4[q][1] += rint_small(y[4 * cc + q].y) << (p * w);
             } else {
@@ -472,7 +634,12 @@ struct B2FArgs {
 // one warp per (i, row, o, p)
 __global__ void __launch_bounds__(32) bsk_to_fourier_warp_kernel(B2FArgs A) {
   __shared__ __align__(16) double2 buf[kM];
+  __shared__ __align__(16) double2 tsm[SZ_TW_SMEM ? kM : 1];
   const int lane = threadIdx.x;
+#if SZ_TW_SMEM
+  for (int e = lane; e < kM; e += 32) tsm[e] = g_t32.tws[e];
+  __syncwarp();
+#endif
   long blk = blockIdx.x;
   const int p = blk % A.P; blk /= A.P;
   const int o = blk % 2; blk /= 2;
@@ -487,7 +654,7 @@ __global__ void __launch_bounds__(32) bsk_to_fourier_warp_kernel(B2FArgs A) {
     limb_split(gsrc[lane + 32 * m + 1024], A.P, A.w, l1);
     x[m] = make_double2(l0[p], l1[p]);
   }
-  fwd_fft32(x, buf, lane);
+  fwd_fft32(x, buf, tsm, lane);
   double2 *dst = A.fbsk + ((((size_t)i * A.P + p) * 2 + o) * 2 + row) * kM;
   const double scale = 1.0 / kM;
 #pragma unroll

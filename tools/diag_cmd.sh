@@ -1,2 +1,2 @@
-python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke3.log 2>&1; echo smoke rc=$? >> gpurun_out/smoke3.log
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_all2.log 2>&1; echo rc=$? >> gpurun_out/gpu_all2.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_gadgets.py -x -q > gpurun_out/diag21.txt 2>&1
+SILENZIO_LIB=paper_2504_17785_b200/libsilenzio.so timeout 300 python tools/time_br.py --batch 8880 --reps 3 >> gpurun_out/diag21.txt 2>&1
