@@ -83,14 +83,14 @@ __device__ __forceinline__ double2 mulw32v(double2 d, int e) {
   }
 }
 
-// Variant switches. All 32 combinations were built (tools/build_warp_variants.sh)
-// and timed on a B200 (profiles/r01_warp_variants.txt): the spread is 31-39 k
-// PBS/s from register allocation alone; the defaults are the fastest.
+// Variant switches. All 64 combinations were built (tools/build_warp_variants.sh)
+// and timed on a B200 (profiles/r01_warp_variants.txt): the spread is 31-40.5 k
+// PBS/s from register allocation and scheduling alone; the defaults are the fastest.
 #ifndef SZ_DFT_DIT
 #define SZ_DFT_DIT 1  // DIT with 6-op FMA butterflies (9 % fewer FP64 ops than DIF)
 #endif
 #ifndef SZ_TW_SMEM
-#define SZ_TW_SMEM 1  // four-step twiddles staged in shared memory (one swizzled table)
+#define SZ_TW_SMEM 0  // four-step twiddles staged in shared memory (one swizzled table)
 #endif
 #ifndef SZ_ACC_FAST
 #define SZ_ACC_FAST 0  // limb recombination without per-limb offset correction
@@ -220,14 +220,20 @@ __device__ __forceinline__ void dft32(double2 (&x)[32]) {
 struct Tables32 {
   double2 tw[32 * 32];
   double2 twT[32 * 32];
-  double2 tws[32 * 32];
+  double2 tws[32 * 33];
 };
 __device__ Tables32 g_t32;
 __constant__ double2 c_twist32[32];
 
 // swizzled index of element (row, col) of a 32 x 32 block of 16-byte values:
 // any 8 consecutive rows (fixed col) or cols (fixed row) hit 8 distinct 16-byte bank groups
-__host__ __device__ constexpr int sw(int row, int col) { return row * 32 + (col ^ (row & 7)); }
+#ifndef SZ_PAD
+#define SZ_PAD 1  // padded rows (stride 33) instead of the XOR swizzle: no per-access index arithmetic
+#endif
+__host__ __device__ constexpr int sw(int row, int col) {
+  return SZ_PAD ? row * 33 + col : row * 32 + (col ^ (row & 7));
+}
+constexpr int kXbuf = SZ_PAD ? 32 * 33 : 1024;  // double2 per transposition buffer
 
 static std::once_flag g_once[64];
 static int g_status[64];
@@ -359,9 +365,9 @@ struct Args {
 
 __host__ __device__ constexpr size_t abar_bytes(int n) { return ((size_t)n * 2 + 15) / 16 * 16; }
 __host__ __device__ constexpr size_t smem_bytes(int n) {
-  return 8 * (size_t)kM * sizeof(double2)    // per-warp transposition buffers (also the ACC copy)
+  return 8 * (size_t)kXbuf * sizeof(double2)  // per-warp transposition buffers (also the ACC copy)
          + 4 * (size_t)kM * sizeof(double2)  // BSK stage: one (i, limb), [o][row][32][32]
-         + (SZ_TW_SMEM ? (size_t)kM * sizeof(double2) : 0)  // twiddle table copy
+         + (SZ_TW_SMEM ? (size_t)kXbuf * sizeof(double2) : 0)  // twiddle table copy
          + kCts * abar_bytes(n)              // modswitched masks
          + 16;                               // mbarrier
 }
@@ -404,20 +410,20 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   __shared__ uint32_t tmem_slot;
   const int n = A.n, w = A.w, blog = A.base_log;
   double2 *xbuf_all = reinterpret_cast<double2 *>(smem);
-  double2 *gbuf = xbuf_all + 8 * kM;
+  double2 *gbuf = xbuf_all + 8 * kXbuf;
   double2 *tsm = gbuf + 4 * kM;  // twiddle copy (SZ_TW_SMEM)
-  unsigned char *abar_base = reinterpret_cast<unsigned char *>(tsm + (SZ_TW_SMEM ? kM : 0));
+  unsigned char *abar_base = reinterpret_cast<unsigned char *>(tsm + (SZ_TW_SMEM ? kXbuf : 0));
   uint64_t *mbar = reinterpret_cast<uint64_t *>(abar_base + kCts * abar_bytes(n));
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int cs = wid & 3, g = wid >> 2;  // ciphertext slot, GLWE component
-  double2 *xbuf = xbuf_all + wid * kM;
+  double2 *xbuf = xbuf_all + wid * kXbuf;
   u64 *accs = reinterpret_cast<u64 *>(xbuf);  // ACC_g copy [2048] for the rotation
   unsigned short *abar = reinterpret_cast<unsigned short *>(abar_base + cs * abar_bytes(n));
 
   if (wid == 0) tmem_alloc(&tmem_slot, kTmemCols);
   if (tid == 32) mbar_init(mbar, 1);
 #if SZ_TW_SMEM
-  for (int e = tid; e < kM; e += kThreads) tsm[e] = g_t32.tws[e];
+  for (int e = tid; e < kXbuf; e += kThreads) tsm[e] = g_t32.tws[e];
 #endif
   tmem_fence_before();
   __syncthreads();
@@ -633,11 +639,11 @@ struct B2FArgs {
 
 // one warp per (i, row, o, p)
 __global__ void __launch_bounds__(32) bsk_to_fourier_warp_kernel(B2FArgs A) {
-  __shared__ __align__(16) double2 buf[kM];
-  __shared__ __align__(16) double2 tsm[SZ_TW_SMEM ? kM : 1];
+  __shared__ __align__(16) double2 buf[kXbuf];
+  __shared__ __align__(16) double2 tsm[SZ_TW_SMEM ? kXbuf : 1];
   const int lane = threadIdx.x;
 #if SZ_TW_SMEM
-  for (int e = lane; e < kM; e += 32) tsm[e] = g_t32.tws[e];
+  for (int e = lane; e < kXbuf; e += 32) tsm[e] = g_t32.tws[e];
   __syncwarp();
 #endif
   long blk = blockIdx.x;
