@@ -377,26 +377,41 @@ __device__ __forceinline__ u64 acc_init(const u64 *v, int j, int bt, int g) {
   const u64 vv = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
   return g ? vv : 0ull;
 }
-// ACC chunk cc (16 columns) = coefficients j = lane + 32 m + 1024 h, m = 4 cc + q (q < 4), h < 2
-__device__ __forceinline__ void acc_ld(uint32_t ta, int cc, u64 (&a)[4][2]) {
-  uint32_t r[16];
-  tmem_ld16(ta + 16 * cc, r);
-  tmem_wait_ld16(r);
+#ifndef SZ_D_ST32
+#define SZ_D_ST32 0  // 32-column TMEM stores of the digit spectra
+#endif
+#ifndef SZ_ACC_CQ
+#define SZ_ACC_CQ 8  // ACC coefficients m per TMEM access chunk (4: 16 columns, 8: 32 columns; 8 measured +2.8 %)
+#endif
+constexpr int kCQ = SZ_ACC_CQ, kNC = 32 / SZ_ACC_CQ;
+// ACC chunk cc (4 kCQ columns) = coefficients j = lane + 32 m + 1024 h, m = kCQ cc + q (q < kCQ), h < 2
+template <int CQ = kCQ>
+__device__ __forceinline__ void acc_ld(uint32_t ta, int cc, u64 (&a)[CQ][2]) {
+  uint32_t r[4 * CQ];
+  if constexpr (CQ == 8) {
+    tmem_ld32(ta + 32 * cc, r);
+    tmem_wait_ld32(r);
+  } else {
+    tmem_ld16(ta + 16 * cc, r);
+    tmem_wait_ld16(r);
+  }
 #pragma unroll
-  for (int q = 0; q < 4; q++)
+  for (int q = 0; q < CQ; q++)
 #pragma unroll
     for (int h = 0; h < 2; h++) a[q][h] = (u64)r[4 * q + 2 * h] | ((u64)r[4 * q + 2 * h + 1] << 32);
 }
-__device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[4][2]) {
-  uint32_t r[16];
+template <int CQ = kCQ>
+__device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[CQ][2]) {
+  uint32_t r[4 * CQ];
 #pragma unroll
-  for (int q = 0; q < 4; q++)
+  for (int q = 0; q < CQ; q++)
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       r[4 * q + 2 * h] = (uint32_t)a[q][h];
       r[4 * q + 2 * h + 1] = (uint32_t)(a[q][h] >> 32);
     }
-  tmem_st16(ta + 16 * cc, r);
+  if constexpr (CQ == 8) tmem_st32(ta + 32 * cc, r);
+  else tmem_st16(ta + 16 * cc, r);
 }
 
 // bits of x + 1.5 * 2^52: round(x) + bits(1.5 * 2^52) for |x| < 2^51 (see rint_small)
@@ -454,12 +469,12 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
     if (id >= A.num_luts) id = 0;
     const u64 *v = A.luts + (size_t)id * kN;
 #pragma unroll 1
-    for (int cc = 0; cc < 8; cc++) {
-      u64 a4[4][2];
+    for (int cc = 0; cc < kNC; cc++) {
+      u64 a4[kCQ][2];
 #pragma unroll
-      for (int q = 0; q < 4; q++)
+      for (int q = 0; q < kCQ; q++)
 #pragma unroll
-        for (int h = 0; h < 2; h++) a4[q][h] = acc_init(v, lane + 32 * (4 * cc + q) + 1024 * h, bt, g);
+        for (int h = 0; h < 2; h++) a4[q][h] = acc_init(v, lane + 32 * (kCQ * cc + q) + 1024 * h, bt, g);
       acc_st(ta_acc, cc, a4);
     }
     tmem_wait_st();
@@ -470,27 +485,27 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
       // ---------------- publish ACC_g for the rotation
       __syncwarp();  // previous inverse FFT's readers of xbuf are done
 #pragma unroll
-      for (int cc = 0; cc < 8; cc++) {
-        u64 a4[4][2];
+      for (int cc = 0; cc < kNC; cc++) {
+        u64 a4[kCQ][2];
         acc_ld(ta_acc, cc, a4);
 #pragma unroll
-        for (int q = 0; q < 4; q++)
+        for (int q = 0; q < kCQ; q++)
 #pragma unroll
-          for (int h = 0; h < 2; h++) accs[lane + 32 * (4 * cc + q) + 1024 * h] = a4[q][h];
+          for (int h = 0; h < 2; h++) accs[lane + 32 * (kCQ * cc + q) + 1024 * h] = a4[q][h];
       }
       __syncwarp();
       // ---------------- digits of X^a ACC_g - ACC_g (a4.1-a4.2), forward FFT
       double2 x[32];
 #pragma unroll
-      for (int cc = 0; cc < 8; cc++) {
-        u64 a4[4][2];
+      for (int cc = 0; cc < kNC; cc++) {
+        u64 a4[kCQ][2];
         acc_ld(ta_acc, cc, a4);
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
+        for (int q = 0; q < kCQ; q++) {
           double dv[2];
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            const int j = lane + 32 * (4 * cc + q) + 1024 * h;
+            const int j = lane + 32 * (kCQ * cc + q) + 1024 * h;
             const int src = (j - a) & (2 * kN - 1);
             const u64 rv = accs[src & (kN - 1)];
             const u64 rot = (src < kN) ? rv : (u64)0 - rv;
@@ -499,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
             // the only level is dropped, as in sz_decomp_next)
             dv[h] = (double)((i64)(rot - a4[q][h] + half_q) >> (64 - blog));
           }
-          x[4 * cc + q] = make_double2(dv[0], dv[1]);
+          x[kCQ * cc + q] = make_double2(dv[0], dv[1]);
         }
       }
       fwd_fft32(x, xbuf, tsm, lane);
@@ -508,12 +523,22 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
         asm volatile("bar.sync %0, %1;" ::"r"(5 + cs), "r"(64) : "memory");
         tmem_fence_after();
       }
+#if SZ_D_ST32
+#pragma unroll
+      for (int jj = 0; jj < 4; jj++) {
+        uint32_t r32[32];
+        pack4(&x[8 * jj], *reinterpret_cast<uint32_t(*)[16]>(&r32[0]));
+        pack4(&x[8 * jj + 4], *reinterpret_cast<uint32_t(*)[16]>(&r32[16]));
+        tmem_st32(ta_dg + 32 * jj, r32);
+      }
+#else
 #pragma unroll
       for (int jj = 0; jj < 8; jj++) {
         uint32_t r16[16];
         pack4(&x[4 * jj], r16);
         tmem_st16(ta_dg + 16 * jj, r16);
       }
+#endif
       tmem_wait_st();
       tmem_fence_before();
       asm volatile("bar.sync %0, %1;" ::"r"(1 + cs), "r"(64) : "memory");  // D^_0 and D^_1 written
@@ -571,30 +596,30 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
         }
         inv_fft32(y, xbuf, tsm, lane);
 #pragma unroll
-        for (int cc = 0; cc < 8; cc++) {
-          u64 a4[4][2];
+        for (int cc = 0; cc < kNC; cc++) {
+          u64 a4[kCQ][2];
           acc_ld(ta_acc, cc, a4);
 #pragma unroll
-          for (int q = 0; q < 4; q++) {
+          for (int q = 0; q < kCQ; q++) {
             if (SZ_ACC_FAST && P == 3 && w == 22) {
               // round(x) << 22p via the 1.5 * 2^52 trick; the magic constant's
               // bits are removed once per CMux (kLimbOffset3, at p = 0)
               if (p == 2) {
-                a4[q][0] += (u64)((uint32_t)limb_bits(y[4 * cc + q].x) << 12) << 32;
-                a4[q][1] += (u64)((uint32_t)limb_bits(y[4 * cc + q].y) << 12) << 32;
+                a4[q][0] += (u64)((uint32_t)limb_bits(y[kCQ * cc + q].x) << 12) << 32;
+                a4[q][1] += (u64)((uint32_t)limb_bits(y[kCQ * cc + q].y) << 12) << 32;
               } else if (p == 1) {
-                a4[q][0] += limb_bits(y[4 * cc + q].x) << 22;
-                a4[q][1] += limb_bits(y[4 * cc + q].y) << 22;
+                a4[q][0] += limb_bits(y[kCQ * cc + q].x) << 22;
+                a4[q][1] += limb_bits(y[kCQ * cc + q].y) << 22;
               } else {
-                a4[q][0] += limb_bits(y[4 * cc + q].x) - kLimbOffset3;
-                a4[q][1] += limb_bits(y[4 * cc + q].y) - kLimbOffset3;
+                a4[q][0] += limb_bits(y[kCQ * cc + q].x) - kLimbOffset3;
+                a4[q][1] += limb_bits(y[kCQ * cc + q].y) - kLimbOffset3;
               }
             } else if (P == 3) {
-              a4[q][0] += rint_small(y[4 * cc + q].x) << (p * w);
-              a4[q][1] += rint_small(y[4 * cc + q].y) << (p * w);
+              a4[q][0] += rint_small(y[kCQ * cc + q].x) << (p * w);
+              a4[q][1] += rint_small(y[kCQ * cc + q].y) << (p * w);
             } else {
-              a4[q][0] += limb_to_torus(y[4 * cc + q].x, p, P, w);
-              a4[q][1] += limb_to_torus(y[4 * cc + q].y, p, P, w);
+              a4[q][0] += limb_to_torus(y[kCQ * cc + q].x, p, P, w);
+              a4[q][1] += limb_to_torus(y[kCQ * cc + q].y, p, P, w);
             }
           }
           acc_st(ta_acc, cc, a4);
@@ -606,14 +631,14 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
     if (live) {
       u64 *out = A.lwe_out + (size_t)c * (kN + 1);
 #pragma unroll 1
-      for (int cc = 0; cc < 8; cc++) {
-        u64 a4[4][2];
+      for (int cc = 0; cc < kNC; cc++) {
+        u64 a4[kCQ][2];
         acc_ld(ta_acc, cc, a4);
 #pragma unroll
-        for (int q = 0; q < 4; q++)
+        for (int q = 0; q < kCQ; q++)
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            const int j = lane + 32 * (4 * cc + q) + 1024 * h;
+            const int j = lane + 32 * (kCQ * cc + q) + 1024 * h;
             if (g == 0) {
               if (j == 0) out[0] = a4[q][h];
               else out[kN - j] = (u64)0 - a4[q][h];
