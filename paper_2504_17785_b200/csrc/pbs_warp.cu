@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int cs = wid & 3, g = wid >> 2;  // ciphertext slot, GLWE component
   double2 *xbuf = xbuf_all + wid * kXbuf;
-  u64 *accs = reinterpret_cast<u64 *>(xbuf);  // ACC_g copy [2048] for the rotation
+  ulonglong2 *accp = reinterpret_cast<ulonglong2 *>(xbuf);  // ACC_g copy as [1024] coefficient pairs
   unsigned short *abar = reinterpret_cast<unsigned short *>(abar_base + cs * abar_bytes(n));
 
   if (wid == 0) tmem_alloc(&tmem_slot, kTmemCols);
@@ -482,19 +482,21 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
 
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
-      // ---------------- publish ACC_g for the rotation
+      // ---------------- publish ACC_g for the rotation, as coefficient pairs
+      // accp[s] = (ACC_g[s], ACC_g[s + 1024]), s < 1024 (one 16-byte access serves both h)
       __syncwarp();  // previous inverse FFT's readers of xbuf are done
 #pragma unroll
       for (int cc = 0; cc < kNC; cc++) {
         u64 a4[kCQ][2];
         acc_ld(ta_acc, cc, a4);
 #pragma unroll
-        for (int q = 0; q < kCQ; q++)
-#pragma unroll
-          for (int h = 0; h < 2; h++) accs[lane + 32 * (kCQ * cc + q) + 1024 * h] = a4[q][h];
+        for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
       }
       __syncwarp();
       // ---------------- digits of X^a ACC_g - ACC_g (a4.1-a4.2), forward FFT
+      // (X^a ACC)[j] = +-ACC[(j - a) mod 2N]: for j0 = lane + 32 m and j1 = j0 + 1024,
+      // src0 = (j0 - a) mod 4096 = 1024 qd + s picks the pair accp[s] for both:
+      //   qd = 0: (+x, +y)   1: (+y, -x)   2: (-x, -y)   3: (-y, +x)
       double2 x[32];
 #pragma unroll
       for (int cc = 0; cc < kNC; cc++) {
@@ -502,19 +504,17 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
         acc_ld(ta_acc, cc, a4);
 #pragma unroll
         for (int q = 0; q < kCQ; q++) {
-          double dv[2];
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int j = lane + 32 * (kCQ * cc + q) + 1024 * h;
-            const int src = (j - a) & (2 * kN - 1);
-            const u64 rv = accs[src & (kN - 1)];
-            const u64 rot = (src < kN) ? rv : (u64)0 - rv;
-            // level-1 balanced digit round((rot - acc) B / q) in [-B/2, B/2): the
-            // arithmetic shift of the half-up-rounded value (C3; the carry out of
-            // the only level is dropped, as in sz_decomp_next)
-            dv[h] = (double)((i64)(rot - a4[q][h] + half_q) >> (64 - blog));
-          }
-          x[kCQ * cc + q] = make_double2(dv[0], dv[1]);
+          const int src0 = (lane + 32 * (kCQ * cc + q) - a) & (2 * kN - 1);
+          const int qd = src0 >> 10;
+          const ulonglong2 pr = accp[src0 & 1023];
+          u64 r0 = (qd & 1) ? pr.y : pr.x, r1 = (qd & 1) ? pr.x : pr.y;
+          if (qd >= 2) r0 = (u64)0 - r0;
+          if (qd == 1 || qd == 2) r1 = (u64)0 - r1;
+          // level-1 balanced digit round((rot - acc) B / q) in [-B/2, B/2): the
+          // arithmetic shift of the half-up-rounded value (C3; the carry out of
+          // the only level is dropped, as in sz_decomp_next)
+          x[kCQ * cc + q] = make_double2((double)((i64)(r0 - a4[q][0] + half_q) >> (64 - blog)),
+                                         (double)((i64)(r1 - a4[q][1] + half_q) >> (64 - blog)));
         }
       }
       fwd_fft32(x, xbuf, tsm, lane);
