@@ -294,6 +294,9 @@ def main():
                               "peak_int8_tops_nominal": 4500.0,
                               "ops_per_ct": ks_ops},
                 "pbs_roofline_pbs_per_s": FP64_PEAK_TFLOPS * 1e12 / flops,
+                # the stricter P = 1 denominator beside it (an approximate single-limb
+                # FFT would need only these flops, but cannot meet the 2^-32 parity bound, DESIGN R20)
+                "frac_vs_p1_flops": (pbs_flops(P.with_(fft_limbs=1)) * B / br_avg_s / 1e12) / FP64_PEAK_TFLOPS,
                 "frac_of_pbs_roofline_whole_step": value / world / (FP64_PEAK_TFLOPS * 1e12 / flops)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

@@ -204,6 +204,41 @@ def test_pbs_multi_lut_ragged_parity(dev):
     assert np.abs(dphi).max() <= PHASE_TOL
 
 
+def test_pbs_config1_full_batch_sampled_parity(dev):
+    """BASELINE configs[1] at the benchmark size and launch configuration
+    (131 072 ciphertexts, 8 LUTs, tensor-core keyswitch + per-wave blind-rotation
+    launches, exactly what bench.py times): every output decrypts to its LUT
+    value, and a sample -- the first and last ciphertext, the edges of the first
+    two waves (592 per wave) and random picks -- is replayed through the oracle
+    one by one (phase within 2^-32)."""
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P, rnd, ok, gk = _setup("A", 0, dev)
+    B = 131072
+    tabs = lut_tables(8, P.p, 0)
+    luts_g = wl.luts_from_tables(tabs, P.p, P.N, dev)
+    ids = lut_ids(B, 8, 1)
+    m = messages(B, P.p, 1)
+    r = lwe_randomness(P, B, 1)
+    ct = wl.encrypt(P, m, r, gk["big_key"], dev)
+    out = silenzio.pbs_batch(ct, torch.from_numpy(ids.astype(np.int32)).to(dev), luts_g, gk["fbsk"], gk["ksk"], P)
+    dec = wl.decode(wl.to_host_u64(silenzio.lwe_phase_batch(out, gk["big_key"])), P.p)
+    assert np.array_equal(dec, tabs[ids, m])
+    wave = 592  # ciphertexts per blind-rotation launch on a 148-SM B200 (4 per SM)
+    sample = np.unique(np.concatenate([[0, 1, wave - 1, wave, 2 * wave - 1, 2 * wave, B - 1],
+                                       np.random.default_rng(5).choice(B, size=9, replace=False)]))
+    ct_s = u64(ct[torch.from_numpy(sample).to(dev)])
+    out_s = u64(out[torch.from_numpy(sample).to(dev)])
+    # the sampled inputs are the oracle's own encryption of the same seeded draws
+    assert np.array_equal(ct_s, oracle.lwe_encrypt(oracle.encode(m[sample], P.p), ok["big_key"],
+                                                   r["mask"][sample], r["noise"][sample]))
+    vs = np.stack([oracle.test_polynomial(oracle.encode(tabs[l], P.p), P.p, P.N) for l in range(8)])
+    out_o = oracle.pbs(ct_s, ids[sample], vs, ok["bsk"], ok["ksk"], P)
+    dphi = oracle.torus_diff(oracle.lwe_phase(out_s, ok["big_key"]), oracle.lwe_phase(out_o, ok["big_key"]))
+    print("config1 full batch: max |dphi| =", int(np.abs(dphi).max()), "bit-exact:",
+          int((out_s == out_o).all(1).sum()), "/", len(sample))
+    assert np.abs(dphi).max() <= PHASE_TOL
+
+
 def test_pbs_single_ciphertext_and_lut_id_clamp(dev):
     from paper_2504_17785_b200 import workload as wl
     P, rnd, ok, gk = _setup("A_SMALLN", 8, dev)
