@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "fft.cuh"
+#include "tmem.cuh"
 
 namespace sz {
 
@@ -162,6 +163,10 @@ __device__ __forceinline__ u64 limb_to_torus_L(double x, int p, int P, int w) {
   return f64_to_torus_L(x);
 }
 
+#ifndef SZ_SETC_TMEM
+#define SZ_SETC_TMEM 1  // digit spectra in TMEM instead of (L2-backed) local memory
+#endif
+
 struct BRLArgs {
   const u64 *lwe_small;
   const u32 *lut_ids;
@@ -186,8 +191,20 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
   unsigned short *abar = reinterpret_cast<unsigned short *>(buf + kML);
   const int t = threadIdx.x;
   const int n = A.n, w = A.w, blog = A.base_log;
-  double2 spec[rows][16];  // thread-private digit spectra (local memory)
-
+  // thread-private digit spectra: in tensor memory when they fit (rows <= 4:
+  // threads t and t + 128 share a lane (warps w, w + 4), columns [0, 256) and
+  // [256, 512); row r, slot sl at column 64 r + 4 sl), else in local memory
+  constexpr bool kTm = SZ_SETC_TMEM && rows <= 4;
+  __shared__ uint32_t tmem_slot;
+  const int wid = t >> 5;
+  if constexpr (kTm) {
+    if (wid == 0) tmem_alloc(&tmem_slot, 512);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+  }
+  const uint32_t ta_spec = kTm ? tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16) + 256 * (wid >> 2) : 0u;
+  double2 spec[kTm ? 1 : rows][16];
   for (long c = blockIdx.x; c < A.count; c += gridDim.x) {
     const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
     for (int i = t; i < n; i += kTL) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2NL);
@@ -232,10 +249,20 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
           }
           fwd_fft_L(x, buf, t);
           const int row = r * L + (lvl - 1);
+          if constexpr (kTm) {
 #pragma unroll
-          for (int sl = 0; sl < 16; sl++) spec[row][sl] = x[sl];
+            for (int j = 0; j < 4; j++) {
+              uint32_t r16[16];
+              pack4(&x[4 * j], r16);
+              tmem_st16(ta_spec + 64 * row + 16 * j, r16);
+            }
+          } else {
+#pragma unroll
+            for (int sl = 0; sl < 16; sl++) spec[row][sl] = x[sl];
+          }
         }
       }
+      if constexpr (kTm) tmem_wait_st();
       __syncthreads();  // all reads of ACC done before the inverse updates it
       // -------- inverse: per output component o, limbs top -> 0
 #pragma unroll 1
@@ -250,13 +277,31 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
 #pragma unroll 1
           for (int row = 0; row < rows; row++) {
             const double2 *G = Gi + ((size_t)row * P + p) * kML;
+            if constexpr (kTm) {
+#pragma unroll
+            for (int qq = 0; qq < 4; qq += 2) {
+              double2 g[8];
+#pragma unroll
+              for (int q = 0; q < 8; q++) g[q] = __ldg(&G[(4 * qq + q) * kTL]);
+              uint32_t d0[16], d1[16];
+              tmem_ld16(ta_spec + 64 * row + 16 * qq, d0);
+              tmem_ld16(ta_spec + 64 * row + 16 * (qq + 1), d1);
+              tmem_wait_ld16x2(d0, d1);
+#pragma unroll
+              for (int q = 0; q < 4; q++) {
+                cmac(y[4 * qq + q], unpack1(d0, q), g[q]);
+                cmac(y[4 * qq + 4 + q], unpack1(d1, q), g[4 + q]);
+              }
+            }
+            } else {
 #pragma unroll
             for (int qq = 0; qq < 4; qq++) {
               double2 g[4];
 #pragma unroll
               for (int q = 0; q < 4; q++) g[q] = __ldg(&G[(4 * qq + q) * kTL]);
 #pragma unroll
-              for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], spec[row][4 * qq + q], g[q]);
+              for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], spec[kTm ? 0 : row][4 * qq + q], g[q]);
+            }
             }
           }
           inv_fft_L(y, buf, t);
@@ -278,6 +323,11 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
       out[j] = val;
     }
     __syncthreads();
+  }
+  if constexpr (kTm) {
+    tmem_fence_before();
+    __syncthreads();
+    if (wid == 0) tmem_dealloc(tmem_slot, 512);
   }
 }
 
@@ -390,7 +440,16 @@ int launch_bsk_to_fourier_large(const u64 *bsk, void *fbsk, const silenzio_param
 constexpr int kNH = 32768;
 constexpr int kMH = 16384;
 constexpr int kLog2_2NH = 16;
-constexpr int kHInFlight = 48;
+// Ciphertexts in flight = one CTA per SM (measured on B200, tools/time_setb.py:
+// 48 in flight (L2-resident state) 107 PBS/s, 96: 160, 148: 265, 296: 269 --
+// the kernel is latency-bound per CTA, so every SM should hold one).
+static long huge_inflight() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+      sms <= 0)
+    return 148;
+  return sms;
+}
 
 __device__ double2 g_FH[4 * 4096];  // F[q][p]
 __constant__ double2 c_CH[16];     // C[m'][q], index m' * 4 + q
@@ -632,13 +691,14 @@ __global__ void __launch_bounds__(256) bsk_to_fourier_huge_kernel(B2FHArgs A) {
 }
 
 size_t blind_rotate_huge_ws_bytes(const silenzio_params *P, size_t count) {
-  const long inflight = (long)count < kHInFlight ? (long)count : kHInFlight;
+  const long cap = huge_inflight();
+  const long inflight = (long)count < cap ? (long)count : cap;
   return (size_t)inflight * brh_ws_per_ct(2 * (int)P->pbs_level);
 }
 
 long blind_rotate_huge_wave(const silenzio_params *P) {
   (void)P;
-  return kHInFlight;
+  return huge_inflight();
 }
 
 int launch_blind_rotate_huge(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
@@ -666,9 +726,10 @@ int launch_blind_rotate_huge(const u64 *lwe_small, const u32 *lut_ids, const u64
   if (!kern) return SILENZIO_ERR_UNSUPPORTED;
   const size_t smem = kML * sizeof(double2) + ((size_t)A.n * 2 + 15) / 16 * 16;
   SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  for (long c0 = 0; c0 < (long)count; c0 += kHInFlight) {
+  const long inflight = huge_inflight();
+  for (long c0 = 0; c0 < (long)count; c0 += inflight) {
     BRHArgs W = A;
-    const long cnt = ((long)count - c0 < kHInFlight) ? (long)count - c0 : kHInFlight;
+    const long cnt = ((long)count - c0 < inflight) ? (long)count - c0 : inflight;
     W.lwe_small = A.lwe_small + (size_t)c0 * (A.n + 1);
     W.lut_ids = A.lut_ids ? A.lut_ids + c0 : nullptr;
     W.lwe_out = A.lwe_out + (size_t)c0 * (kNH + 1);
