@@ -377,6 +377,9 @@ __device__ __forceinline__ u64 acc_init(const u64 *v, int j, int bt, int g) {
   const u64 vv = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
   return g ? vv : 0ull;
 }
+#ifndef SZ_PUB_FUSED
+#define SZ_PUB_FUSED 0  // last limb also writes the rotation copy: correct, measured -25 % (codegen)
+#endif
 #ifndef SZ_D_ST32
 #define SZ_D_ST32 0  // 32-column TMEM stores of the digit spectra
 #endif
@@ -476,6 +479,10 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
 #pragma unroll
         for (int h = 0; h < 2; h++) a4[q][h] = acc_init(v, lane + 32 * (kCQ * cc + q) + 1024 * h, bt, g);
       acc_st(ta_acc, cc, a4);
+#if SZ_PUB_FUSED
+#pragma unroll
+      for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
+#endif
     }
     tmem_wait_st();
     __syncthreads();  // abar visible
@@ -484,6 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
       const int a = abar[i];
       // ---------------- publish ACC_g for the rotation, as coefficient pairs
       // accp[s] = (ACC_g[s], ACC_g[s + 1024]), s < 1024 (one 16-byte access serves both h)
+#if !SZ_PUB_FUSED
       __syncwarp();  // previous inverse FFT's readers of xbuf are done
 #pragma unroll
       for (int cc = 0; cc < kNC; cc++) {
@@ -492,6 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
 #pragma unroll
         for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
       }
+#endif
       __syncwarp();
       // ---------------- digits of X^a ACC_g - ACC_g (a4.1-a4.2), forward FFT
       // (X^a ACC)[j] = +-ACC[(j - a) mod 2N]: for j0 = lane + 32 m and j1 = j0 + 1024,
@@ -595,6 +604,9 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
           }
         }
         inv_fft32(y, xbuf, tsm, lane);
+#if SZ_PUB_FUSED
+        if (p == 0) __syncwarp();  // the last limb also publishes the new ACC into xbuf
+#endif
 #pragma unroll
         for (int cc = 0; cc < kNC; cc++) {
           u64 a4[kCQ][2];
@@ -623,6 +635,12 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
             }
           }
           acc_st(ta_acc, cc, a4);
+#if SZ_PUB_FUSED
+          if (p == 0) {
+#pragma unroll
+            for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
+          }
+#endif
         }
         tmem_wait_st();
       }
