@@ -285,7 +285,11 @@ def main():
     br_avg_s = float(np.mean(br_ms)) / 1e3
     achieved = flops * B / br_avg_s / 1e12
     roofline = {"bound": "alu", "pipe": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                # dram__bytes_read.sum + dram__bytes_write.sum of one full-wave launch (592 ciphertexts) from
+                # the committed ncu --set full capture (151.5 MB read = the 146 MB Fourier BSK once per wave
+                # + inputs; 6.1 MB written): per launch, HBM is far from the bound
+                "traffic": 157.6e6, "traffic_source": "profiles/r01_ncu_blind_rotate_warp.txt (per launch)",
                 "kernel": "blind_rotate_warp_kernel<3>", "algorithmic_flops_per_pbs": flops,
                 "kernel_ms": float(np.mean(br_ms)), "keyswitch_ms": float(np.mean(ks_ms)),
                 "peak_source": "measured DFMA burst (tools/microbench/mb.cu, profiles/r01_microbench_b200.txt)",
