@@ -74,8 +74,8 @@ size_t silenzio_fourier_bsk_bytes(const silenzio_params *params);
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *params, size_t count);
 
 /* Number of kernel launches silenzio_pbs_batch makes for `count` ciphertexts:
- * the keyswitch (tensor-core path: KSK byte-plane preparation + one GEMM per
- * 65535 x 128 ciphertexts; CUDA-core path: one) plus one blind rotation per
+ * the keyswitch (tensor-core path: KSK byte-plane preparation + digit matrix
+ * and GEMM per 65535 x 128 ciphertexts; CUDA-core path: one) plus one blind rotation per
  * resident wave (all CTAs of a wave sweep the Fourier BSK together).
  * -1 if the parameters are unsupported. */
 long silenzio_pbs_launch_count(const silenzio_params *params, size_t count);
@@ -91,17 +91,18 @@ long silenzio_pbs_launch_count(const silenzio_params *params, size_t count);
 int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fourier_bsk,
                             const silenzio_params *params, void *stream);
 
-/* Device bytes of the keyswitch workspace (the KSK split into byte planes in
- * the tensor-core operand layout); 0 when the parameters do not admit the
- * tensor-core path (digits must fit int8: ks_base_log <= 7, and
- * ks_in_dim * l_ks * 2^(ks_base_log-1) * 255 < 2^31). Independent of count. */
+/* Device bytes of the keyswitch workspace for `count` ciphertexts: the KSK
+ * split into byte planes and the int8 digit matrix, both in the tensor-core
+ * operand layout (63 MB + count x 10 KiB at set A); 0 when the parameters do
+ * not admit the tensor-core path (digits must fit int8: ks_base_log <= 7, and
+ * ks_in_dim * l_ks * 2^(ks_base_log-1) * 255 < 2^31). */
 size_t silenzio_keyswitch_workspace_bytes(const silenzio_params *params, size_t count);
 
 /* LWE keyswitch big key -> small key.
  *  lwe_in  [count][ks_in_dim+1], ksk [ks_in_dim][l_ks][n+1], lwe_out [count][n+1].
  *  out = (0,...,0,b) - sum_j sum_t Dec_t(a_j) * KSK[j][t], exact mod 2^64.
- *  workspace: >= silenzio_keyswitch_workspace_bytes device bytes, 16-byte
- *  aligned, or NULL. With a workspace the product runs on the tensor cores
+ *  workspace: >= silenzio_keyswitch_workspace_bytes(params, count) device
+ *  bytes, 16-byte aligned, or NULL. With a workspace the product runs on the tensor cores
  *  (tcgen05 int8 MMA over the KSK byte planes, re-derived from ksk on every
  *  call); without one (or when the byte count is 0) on the CUDA cores. Both
  *  are exact, so the result is identical. */

@@ -20,7 +20,7 @@ int launch_bsk_to_fourier_huge(const u64 *, void *, const silenzio_params *, cud
 size_t blind_rotate_huge_ws_bytes(const silenzio_params *, size_t);
 long blind_rotate_huge_wave(const silenzio_params *);
 int launch_keyswitch(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, cudaStream_t);
-size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log);
+size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log, size_t count);
 int launch_keyswitch_tc(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, void *, cudaStream_t);
 int launch_lwe_encrypt(const u64 *, const i64 *, const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_lwe_phase(const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
@@ -119,10 +119,9 @@ size_t silenzio_blind_rotate_workspace_bytes(const silenzio_params *P, size_t co
 }
 
 size_t silenzio_keyswitch_workspace_bytes(const silenzio_params *P, size_t count) {
-  (void)count;
   if (check_params(P) != SILENZIO_OK || check_ks_params(P) != SILENZIO_OK) return 0;
   return round_up(keyswitch_tc_workspace_bytes((int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_level,
-                                               (int)P->ks_base_log), 256);
+                                               (int)P->ks_base_log, count), 256);
 }
 
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *P, size_t count) {
@@ -211,8 +210,8 @@ long silenzio_pbs_launch_count(const silenzio_params *P, size_t count) {
                    : P->poly_size == 32768 ? blind_rotate_huge_wave(P)
                                            : blind_rotate_wave(P);
   if (wave <= 0) return -1;
-  // keyswitch: byte-plane preparation + one GEMM launch per 65535 row tiles (tensor cores), else one launch
-  const long ks = silenzio_keyswitch_workspace_bytes(P, count) > 0 ? 1 + (long)((count + 65535L * 128 - 1) / (65535L * 128)) : 1;
+  // keyswitch: byte-plane preparation + (digit matrix + GEMM) per 65535 row tiles (tensor cores), else one launch
+  const long ks = silenzio_keyswitch_workspace_bytes(P, count) > 0 ? 1 + 2 * (long)((count + 65535L * 128 - 1) / (65535L * 128)) : 1;
   return ks + (long)((count + wave - 1) / wave);  // + one blind rotation per wave
 }
 

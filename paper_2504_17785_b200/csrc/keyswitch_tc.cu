@@ -15,11 +15,13 @@
 //   * B (byte planes) is pre-arranged once per call (ks_planes_kernel) in the
 //     tensor-core core-matrix layout, so each K-stage is one contiguous bulk
 //     copy (cp.async.bulk, mbarrier completion);
-//   * A (digits) is produced by the threads: each thread decomposes 16 input
-//     coefficients of one ciphertext per stage straight into the core-matrix
-//     layout (no HBM round trip for the digit matrix);
-//   * one thread issues the l MMAs of a stage (M=128, N=256, K=32 each) and
-//     commits them to the stage's "empty" mbarrier; 3 stages in flight;
+//   * A (signed digits) is decomposed once per call (ks_digits_kernel) into the
+//     same core-matrix layout, per 128-row tile and K-stage, so each stage of
+//     both operands is two contiguous bulk copies; the 24 column-block CTAs of a
+//     row tile (adjacent in launch order) re-read it from L2;
+//   * one thread streams the stages (mbarrier expect-tx) and issues the l MMAs
+//     of each (M=128, N=256, K=32 each), committing them to the stage's "empty"
+//     mbarrier; 3 stages in flight;
 //   * the epilogue reads the int32 accumulators from TMEM (thread = ciphertext
 //     row), recombines sum_b C_b << 8b, subtracts from the body column.
 //
@@ -86,6 +88,46 @@ __global__ void ks_planes_kernel(const u64 *ksk, unsigned char *planes, int K, i
   }
 }
 
+// ------------------------------------------------------------ digit matrix
+// digits[row_tile][stage][a_tile]: row r of the tile = ciphertext 128 rt + r,
+// K index k = jj l + t - 1 for coefficient j = 32 stage + jj (signed digit of
+// level t, C3 decomposition). One thread per (ciphertext, stage, half of the
+// stage's 32 coefficients): 16 coefficients -> 16 l digit bytes.
+template <int L>
+__global__ void ks_digits_kernel(const u64 *in, unsigned char *digits, long count, int rows_padded, int in_dim,
+                                 int base_log) {
+  constexpr int KST = stage_k(L);
+  const int nst = in_dim / kJ;
+  const long total = (long)rows_padded * nst * 2;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const int h = (int)(e & 1);
+    long rest = e >> 1;
+    const long row = rest % rows_padded;
+    const int st = (int)(rest / rows_padded);
+    const bool live = row < count;
+    const u64 *arow = in + (size_t)(live ? row : 0) * (in_dim + 1) + kJ * st + 16 * h;
+    uint32_t w[4 * L];
+#pragma unroll
+    for (int q = 0; q < 4 * L; q++) w[q] = 0;
+#pragma unroll
+    for (int jj = 0; jj < 16; jj++) {
+      u64 rr = sz_decomp_round(live ? __ldg(arow + jj) : 0ull, base_log, L);
+#pragma unroll
+      for (int t = L; t >= 1; t--) {
+        const int d = (int)sz_decomp_next(rr, base_log);
+        const int k = jj * L + (t - 1);
+        w[k >> 2] |= (uint32_t)(d & 0xff) << (8 * (k & 3));
+      }
+    }
+    unsigned char *tile = digits + ((size_t)(row / kRows) * nst + st) * a_tile(L);
+    const int r = (int)(row % kRows);
+#pragma unroll
+    for (int c = 0; c < L; c++)
+      *reinterpret_cast<uint4 *>(tile + cm_off(r, 16 * (h * L + c), KST)) =
+          make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
+  }
+}
+
 // --------------------------------------------------------------- primitives
 __device__ __forceinline__ void mbar_init(uint64_t *m, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(m)), "r"(count) : "memory");
@@ -100,6 +142,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *m, uint32_t phase) {
       "}\n" ::"r"(smem_u32(m)),
       "r"(phase)
       : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *m, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void *dst, const void *src, uint32_t bytes, uint64_t *m) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(m))
+               : "memory");
 }
 __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *m) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(m)), "r"(bytes) : "memory");
@@ -135,6 +186,7 @@ __device__ __forceinline__ void mma_commit(uint64_t *m) {
 struct Args {
   const u64 *in;                // [count][in_dim+1]
   const unsigned char *planes;  // [ncb][nst][b_tile]
+  const unsigned char *digits;  // [row tiles][nst][a_tile]
   u64 *out;                     // [count][n+1]
   long count;
   int in_dim, n1, base_log, level;
@@ -173,75 +225,37 @@ __global__ void __launch_bounds__(kThreads, 1) keyswitch_tc_kernel(Args A) {
   const uint32_t tmem_d = tmem_slot;
   const unsigned char *Bg = A.planes + (size_t)cb * nst * b_tile(L);
 
-  // producer role of this thread for A: ciphertext row r, half h of the stage's 32 coefficients
-  const int r = tid & (kRows - 1), h = tid >> 7;
-  const long crow = row0 + r;
-  const bool live = crow < A.count;
-  const u64 *arow = A.in + (size_t)(live ? crow : 0) * (A.in_dim + 1);
-
-  if (tid == 0)
-    for (int p = 0; p < kStages - 1 && p < nst; p++) bulk_load(Bs + p * b_tile(L), Bg + (size_t)p * b_tile(L), b_tile(L), &full[p]);
-
-  // this thread's 16 input coefficients of the current stage; the next stage's
-  // are loaded one iteration ahead so their latency hides behind this stage
-  u64 av[16];
+  const unsigned char *Ag = A.digits + (size_t)blockIdx.y * nst * a_tile(L);
+  if (tid == 0) {
+    // one thread streams both operands stage by stage and issues the MMAs,
+    // kStages - 1 stages ahead of the tensor core
+    for (int it = 0; it < nst + kStages - 1; it++) {
+      if (it < nst) {
+        const int s = it % kStages;
+        if (it >= kStages) mbar_wait(&empty[s], ((it / kStages) - 1) & 1);  // MMAs of stage it - kStages done
+        mbar_expect_tx(&full[s], a_tile(L) + b_tile(L));
+        bulk_copy(As + s * a_tile(L), Ag + (size_t)it * a_tile(L), a_tile(L), &full[s]);
+        bulk_copy(Bs + s * b_tile(L), Bg + (size_t)it * b_tile(L), b_tile(L), &full[s]);
+      }
+      const int kc = it - (kStages - 1);
+      if (kc >= 0) {
+        const int s = kc % kStages;
+        mbar_wait(&full[s], (kc / kStages) & 1);
+        tmem_fence_after();
+        const unsigned char *at = As + s * a_tile(L);
+        const unsigned char *bt = Bs + s * b_tile(L);
 #pragma unroll
-  for (int q = 0; q < 16; q++) av[q] = live ? __ldg(arow + 16 * h + q) : 0ull;
-
-  for (int ks = 0; ks < nst; ks++) {
-    u64 nx[16];
-#pragma unroll
-    for (int q = 0; q < 16; q++) nx[q] = (live && ks + 1 < nst) ? __ldg(arow + kJ * (ks + 1) + 16 * h + q) : 0ull;
-    const int s = ks % kStages;
-    // prefetch B of stage ks + kStages - 1 into the buffer MMA ks - 1 is reading
-    const int kp = ks + kStages - 1;
-    if (tid == 0 && kp < nst) {
-      const int sp = kp % kStages;
-      if (kp >= kStages) mbar_wait(&empty[sp], ((kp / kStages) - 1) & 1);
-      bulk_load(Bs + sp * b_tile(L), Bg + (size_t)kp * b_tile(L), b_tile(L), &full[sp]);
-    }
-    // A buffer s was last read by MMA ks - kStages
-    if (ks >= kStages) mbar_wait(&empty[s], ((ks / kStages) - 1) & 1);
-    {
-      // 16 coefficients j = 32 ks + 16 h + jj -> 16 l signed digits, k = jj l + t - 1 (+ 16 h l)
-      uint32_t w[4 * L];  // 16 l bytes
-#pragma unroll
-      for (int q = 0; q < 4 * L; q++) w[q] = 0;
-#pragma unroll
-      for (int jj = 0; jj < 16; jj++) {
-        u64 rr = sz_decomp_round(av[jj], A.base_log, L);
-#pragma unroll
-        for (int t = L; t >= 1; t--) {
-          const int d = (int)sz_decomp_next(rr, A.base_log);
-          const int k = jj * L + (t - 1);
-          w[k >> 2] |= (uint32_t)(d & 0xff) << (8 * (k & 3));
+        for (int q = 0; q < L; q++) {  // K = 32 per MMA: core-matrix chunks 2q, 2q + 1
+          const uint64_t ad = smem_desc(at + q * 256, 128, (KST / 16) * 128);
+          const uint64_t bd = smem_desc(bt + q * 256, 128, (KST / 16) * 128);
+          mma_i8(tmem_d, ad, bd, (kc > 0 || q > 0) ? 1u : 0u);
         }
+        mma_commit(&empty[s]);
+        if (kc == nst - 1) mma_commit(done);
       }
-      unsigned char *at = As + s * a_tile(L);
-#pragma unroll
-      for (int c = 0; c < L; c++)
-        *reinterpret_cast<uint4 *>(at + cm_off(r, 16 * (h * L + c), KST)) =
-            make_uint4(w[4 * c], w[4 * c + 1], w[4 * c + 2], w[4 * c + 3]);
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> tensor core
-    __syncthreads();
-    if (tid == 0) {
-      mbar_wait(&full[s], (ks / kStages) & 1);
-      tmem_fence_after();
-      const unsigned char *at = As + s * a_tile(L);
-      const unsigned char *bt = Bs + s * b_tile(L);
-#pragma unroll
-      for (int q = 0; q < L; q++) {  // K = 32 per MMA: core-matrix chunks 2q, 2q + 1
-        const uint64_t ad = smem_desc(at + q * 256, 128, (KST / 16) * 128);
-        const uint64_t bd = smem_desc(bt + q * 256, 128, (KST / 16) * 128);
-        mma_i8(tmem_d, ad, bd, (ks > 0 || q > 0) ? 1u : 0u);
-      }
-      mma_commit(&empty[s]);
-      if (ks == nst - 1) mma_commit(done);
-    }
-#pragma unroll
-    for (int q = 0; q < 16; q++) av[q] = nx[q];
   }
+  __syncwarp();
   // ---- epilogue: thread (warp w, lane) owns ciphertext row 32 (w % 4) + lane,
   // output columns 16 (w / 4) .. + 15 of this CTA's 32
   mbar_wait(done, 0);
@@ -284,10 +298,15 @@ static bool ks_tc_applicable(int in_dim, int level, int base_log) {
   return kst::smem_bytes(level) <= 227 * 1024;
 }
 
-size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log) {
-  if (!ks_tc_applicable(in_dim, level, base_log)) return 0;
+// workspace: KSK byte planes [ncb][nst][b_tile], then the digit matrix [row tiles][nst][a_tile]
+static size_t ks_planes_bytes(int in_dim, int n, int level) {
   const size_t ncb = (size_t)(n + 1 + kst::kCols - 1) / kst::kCols;
   return ncb * (size_t)in_dim * level * kst::kN;
+}
+size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log, size_t count) {
+  if (!ks_tc_applicable(in_dim, level, base_log)) return 0;
+  const size_t rows = (count + kst::kRows - 1) / kst::kRows * kst::kRows;
+  return ks_planes_bytes(in_dim, n, level) + rows * (size_t)in_dim * level;
 }
 
 int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, int in_dim, int n, int base_log,
@@ -297,6 +316,7 @@ int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, i
   const int n1 = n + 1, K = in_dim * level;
   const int ncb = (n1 + kst::kCols - 1) / kst::kCols;
   unsigned char *planes = reinterpret_cast<unsigned char *>(workspace);
+  unsigned char *digits = planes + ks_planes_bytes(in_dim, n, level);
   {
     const long total = (long)ncb * (K / kst::stage_k(level)) * kst::kCols * (kst::stage_k(level) / 16);
     const int threads = 256;
@@ -316,10 +336,28 @@ int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, i
   }
   const size_t smem = kst::smem_bytes(level);
   SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void (*dkern)(const u64 *, unsigned char *, long, int, int, int) = nullptr;
+  switch (level) {
+    case 1: dkern = kst::ks_digits_kernel<1>; break;
+    case 2: dkern = kst::ks_digits_kernel<2>; break;
+    case 3: dkern = kst::ks_digits_kernel<3>; break;
+    case 4: dkern = kst::ks_digits_kernel<4>; break;
+    case 5: dkern = kst::ks_digits_kernel<5>; break;
+    case 6: dkern = kst::ks_digits_kernel<6>; break;
+    default: return SILENZIO_ERR_UNSUPPORTED;
+  }
   const size_t max_rows = (size_t)65535 * kst::kRows;  // grid.y limit per launch
   for (size_t c0 = 0; c0 < count; c0 += max_rows) {
     const size_t cnt = count - c0 < max_rows ? count - c0 : max_rows;
-    kst::Args A{in + c0 * (size_t)(in_dim + 1), planes, out + c0 * (size_t)n1, (long)cnt, in_dim, n1, base_log, level};
+    const int rows_padded = (int)((cnt + kst::kRows - 1) / kst::kRows * kst::kRows);
+    {
+      const long total = (long)rows_padded * (in_dim / kst::kJ) * 2;
+      const long blocks = (total + 255) / 256;
+      dkern<<<(unsigned)(blocks < 65535L * 64 ? blocks : 65535L * 64), 256, 0, stream>>>(
+          in + c0 * (size_t)(in_dim + 1), digits, (long)cnt, rows_padded, in_dim, base_log);
+      SZ_LAUNCH_OK();
+    }
+    kst::Args A{in + c0 * (size_t)(in_dim + 1), planes, digits, out + c0 * (size_t)n1, (long)cnt, in_dim, n1, base_log, level};
     dim3 grid((unsigned)ncb, (unsigned)((cnt + kst::kRows - 1) / kst::kRows));
     kern<<<grid, kst::kThreads, smem, stream>>>(A);
     SZ_LAUNCH_OK();

@@ -15,7 +15,7 @@ for B in (16384, 131072):
     ct = torch.randint(-2 ** 62, 2 ** 62, (B, P.big_dim + 1), dtype=torch.int64, device=dev)
     ref = None
     for tc in (True, False):
-        ws = torch.empty(silenzio.keyswitch_workspace_bytes(P), dtype=torch.uint8, device=dev) if tc else None
+        ws = torch.empty(silenzio.keyswitch_workspace_bytes(P, B), dtype=torch.uint8, device=dev) if tc else None
         out = silenzio.keyswitch_batch(ct, gk["ksk"], P, tensor_cores=tc, workspace=ws)
         torch.cuda.synchronize()
         ts = []
