@@ -152,6 +152,33 @@ def shift2msbs_pm(X, moduli, w: int, Gamma: int):
     return s * Yplus, shift
 
 
+def exact_block_scale(x, shift: int):
+    """Exact block scaling by the common exponent `shift` (SURVEY §8(f) #4, P:623:
+    "an exact block-scaling implementation"; reading R22): x / 2^shift rounded
+    toward zero for shift >= 0, x * 2^-shift for shift < 0."""
+    x = np.asarray(x, dtype=np.int64)
+    if shift >= 0:
+        return np.sign(x) * (np.abs(x) >> shift)
+    return x << (-shift)
+
+
+def exact_block_shift(x, Gamma: int) -> int:
+    """Exponent of exact block scaling to Gamma signed bits: the tensor maximum
+    keeps Gamma - 1 magnitude bits, bitlen(max |x|) - (Gamma - 1) (R22)."""
+    m = int(np.abs(np.asarray(x, dtype=np.int64)).max(initial=0))
+    return m.bit_length() - (Gamma - 1)
+
+
+def shift2msbs_approx_error(x, moduli, w: int, Gamma: int):
+    """|Shift2MSBs+-(x) - exact block scaling of x to Gamma bits| per element
+    (SURVEY §8(f) #4). Returns (errors, Y, exact, exact_shift)."""
+    x = np.asarray(x, dtype=np.int64)
+    Y, _ = shift2msbs_pm(to_rns(x, moduli), moduli, w, Gamma)
+    s = exact_block_shift(x, Gamma)
+    E = exact_block_scale(x, s)
+    return np.abs(Y - E), Y, E, s
+
+
 # -------------------------------------------------------- IntCELossDeriv
 def round_half_even(x):
     return np.rint(x).astype(np.int64)

@@ -133,3 +133,32 @@ def test_ce_gradient_gamma3_kappa0_closed_form():
     Ehat = np.rint((e1 + 1) / (S + 1)).astype(np.int64)
     Ehat = Ehat - Y * Ehat.sum(axis=1, keepdims=True)
     assert np.array_equal(E, np.sign(Ehat))
+
+
+def test_exact_block_scale_and_shift2msbs_error_statistic():
+    """Shift2MSBs+- vs exact block scaling (R22).
+    Pins: exact block scaling is x / 2^s toward zero (closed form on powers of
+    two and their negatives); tensors that already fit Gamma bits are returned
+    unchanged by Shift2MSBs+- when every magnitude is a single MRNS digit
+    (|x| < m_0 = 5; larger values inside Gamma bits are digit sums, R11, so
+    not exact); on the config-4 shaped synthetic
+    tensors the error stays small (the statistic DESIGN.md reports)."""
+    from synth import streams
+    x = np.array([0, 1, -1, 2 ** 10, -(2 ** 10), 2 ** 10 + 2 ** 9 - 1, -(2 ** 10 + 1)])
+    assert G.exact_block_shift(x, 4) == 11 - 3
+    assert np.array_equal(G.exact_block_scale(x, 8), [0, 0, 0, 4, -4, 5, -4])
+    assert np.array_equal(G.exact_block_scale(np.array([3, -3]), -2), [12, -12])
+    base = [5, 7, 9, 11, 13, 16]
+    small = np.arange(-4, 5)
+    e, Y, E, s = G.shift2msbs_approx_error(small, base, 4, 4)
+    assert s == 0 and np.array_equal(E, small) and e.max() == 0
+    rng = streams(62)["messages"]
+    X = rng.integers(-8, 8, size=(64, 784))
+    W = rng.integers(-8, 8, size=(784, 128))
+    A2 = rng.integers(-8, 8, size=(64, 128))
+    W2 = rng.integers(-8, 8, size=(128, 10))
+    for T, mean_bound, max_bound in ((X @ W, 0.25, 1), (A2 @ W2, 0.75, 2)):
+        e, Y, E, s = G.shift2msbs_approx_error(T, base, 4, 4)
+        assert np.abs(Y).max() <= 7 and np.abs(E).max() <= 7
+        print("Shift2MSBs+- vs exact block scaling: exact shift", s, "mean |err|", e.mean(), "max", e.max())
+        assert e.mean() <= mean_bound and e.max() <= max_bound
