@@ -75,8 +75,9 @@ size_t silenzio_pbs_workspace_bytes(const silenzio_params *params, size_t count)
 
 /* Number of kernel launches silenzio_pbs_batch makes for `count` ciphertexts:
  * the keyswitch (tensor-core path: KSK byte-plane preparation + digit matrix
- * and GEMM per 65535 x 128 ciphertexts; CUDA-core path: one) plus one blind rotation per
- * resident wave (all CTAs of a wave sweep the Fourier BSK together).
+ * and GEMM per 65535 x 128 ciphertexts; CUDA-core path: one) plus the blind
+ * rotation (N = 2048, level 1: one persistent launch; otherwise one launch per
+ * resident wave, all CTAs of a wave sweeping the Fourier BSK together).
  * -1 if the parameters are unsupported. */
 long silenzio_pbs_launch_count(const silenzio_params *params, size_t count);
 

@@ -10,6 +10,7 @@ int launch_blind_rotate(const u64 *, const u32 *, const u64 *, u32, const void *
                         const silenzio_params *, cudaStream_t);
 int launch_bsk_to_fourier(const u64 *, void *, const silenzio_params *, cudaStream_t);
 long blind_rotate_wave(const silenzio_params *);
+long blind_rotate_launches(const silenzio_params *, size_t);
 int launch_blind_rotate_large(const u64 *, const u32 *, const u64 *, u32, const void *, u64 *, size_t,
                               const silenzio_params *, cudaStream_t);
 int launch_bsk_to_fourier_large(const u64 *, void *, const silenzio_params *, cudaStream_t);
@@ -206,13 +207,17 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
 long silenzio_pbs_launch_count(const silenzio_params *P, size_t count) {
   if (check_params(P) != SILENZIO_OK || check_br_supported(P) != SILENZIO_OK) return -1;
   if (count == 0) return 0;
-  const long wave = P->poly_size == 8192    ? blind_rotate_large_wave(P)
-                   : P->poly_size == 32768 ? blind_rotate_huge_wave(P)
-                                           : blind_rotate_wave(P);
-  if (wave <= 0) return -1;
+  long br;
+  if (P->poly_size == 2048) {
+    br = blind_rotate_launches(P, count);  // one persistent launch (set A) or one per wave
+  } else {
+    const long wave = P->poly_size == 8192 ? blind_rotate_large_wave(P) : blind_rotate_huge_wave(P);
+    br = wave <= 0 ? -1 : (long)((count + wave - 1) / wave);  // one per resident wave
+  }
+  if (br < 0) return -1;
   // keyswitch: byte-plane preparation + (digit matrix + GEMM) per 65535 row tiles (tensor cores), else one launch
   const long ks = silenzio_keyswitch_workspace_bytes(P, count) > 0 ? 1 + 2 * (long)((count + 65535L * 128 - 1) / (65535L * 128)) : 1;
-  return ks + (long)((count + wave - 1) / wave);  // + one blind rotation per wave
+  return ks + br;
 }
 
 size_t silenzio_pbs_host_workspace_bytes(const silenzio_params *P, size_t chunk) {

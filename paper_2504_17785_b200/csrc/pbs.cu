@@ -660,6 +660,8 @@ static int plan_blind_rotate(const silenzio_params *P, BRPlan *plan) {
 // N = 2048, level-1 gadget: the warp-FFT kernel of pbs_warp.cu (own Fourier-BSK layout)
 bool blind_rotate_warp_supported(const silenzio_params *P);
 long blind_rotate_warp_wave();
+long blind_rotate_warp_launches(size_t count);
+long blind_rotate_wave(const silenzio_params *P);
 int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
                              const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
                              cudaStream_t stream);
@@ -669,6 +671,13 @@ static bool use_warp(const silenzio_params *) { return false; }
 #else
 static bool use_warp(const silenzio_params *P) { return blind_rotate_warp_supported(P); }
 #endif
+
+// number of blind-rotation kernel launches for `count` ciphertexts
+long blind_rotate_launches(const silenzio_params *P, size_t count) {
+  if (use_warp(P)) return blind_rotate_warp_launches(count);
+  const long wave = blind_rotate_wave(P);
+  return wave <= 0 ? -1 : (long)((count + wave - 1) / wave);
+}
 
 long blind_rotate_wave(const silenzio_params *P) {
   if (use_warp(P)) return blind_rotate_warp_wave();
