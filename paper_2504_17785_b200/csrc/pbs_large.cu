@@ -167,6 +167,10 @@ __device__ __forceinline__ u64 limb_to_torus_L(double x, int p, int P, int w) {
 #define SZ_SETC_TMEM 1  // digit spectra in TMEM instead of (L2-backed) local memory
 #endif
 
+#ifndef SZ_SETC_MAC2
+#define SZ_SETC_MAC2 0  // measured 1.66k vs 2.80k PBS/s (spills in the hot loop); MAC: all rows' BSK loads of a slot group in flight together
+#endif
+
 struct BRLArgs {
   const u64 *lwe_small;
   const u32 *lut_ids;
@@ -274,6 +278,28 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
           double2 y[16];
 #pragma unroll
           for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
+#if SZ_SETC_MAC2
+          if constexpr (kTm) {
+            // all rows of a 4-slot group loaded together: rows x 4 BSK loads in
+            // flight per thread (the MAC is bound by their L2 latency)
+#pragma unroll
+            for (int qq = 0; qq < 4; qq++) {
+              double2 g[rows][4];
+#pragma unroll
+              for (int row = 0; row < rows; row++)
+#pragma unroll
+                for (int q = 0; q < 4; q++) g[row][q] = __ldg(&Gi[((size_t)row * P + p) * kML + (4 * qq + q) * kTL]);
+#pragma unroll
+              for (int row = 0; row < rows; row++) {
+                uint32_t d[16];
+                tmem_ld16(ta_spec + 64 * row + 16 * qq, d);
+                tmem_wait_ld16(d);
+#pragma unroll
+                for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], unpack1(d, q), g[row][q]);
+              }
+            }
+          } else
+#endif
 #pragma unroll 1
           for (int row = 0; row < rows; row++) {
             const double2 *G = Gi + ((size_t)row * P + p) * kML;

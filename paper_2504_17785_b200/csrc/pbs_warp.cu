@@ -127,8 +127,9 @@ struct T32 {
 // when INV), 6 FP64 instructions when nontrivial: with W^e = i^q e^{i theta},
 //   e^{i theta} b = cos (b.x - tan b.y, b.y + tan b.x) = sin (cot b.x - b.y, cot b.y + b.x)
 // and the cos / sin scale folds into the four output FMAs.
+// R: pending-scale ratio s_b / s_a (1 unless inputs carry factored-out twist scales)
 template <int E, bool INV>
-__device__ __forceinline__ void bfly(double2 &a, double2 &b) {
+__device__ __forceinline__ void bfly(double2 &a, double2 &b, double R = 1.0) {
   constexpr int e = INV ? ((32 - (E & 31)) & 31) : (E & 31);
   constexpr int q = e >> 3, r = e & 7;
   if constexpr (r == 0) {
@@ -137,9 +138,16 @@ __device__ __forceinline__ void bfly(double2 &a, double2 &b) {
     else if constexpr (q == 1) t = make_double2(-b.y, b.x);
     else if constexpr (q == 2) t = make_double2(-b.x, -b.y);
     else t = make_double2(b.y, -b.x);
-    const double2 na = cadd(a, t), nb = csub(a, t);
-    a = na;
-    b = nb;
+    if (R == 1.0) {
+      const double2 na = cadd(a, t), nb = csub(a, t);
+      a = na;
+      b = nb;
+    } else {
+      const double2 na = make_double2(fma(R, t.x, a.x), fma(R, t.y, a.y));
+      const double2 nb = make_double2(fma(-R, t.x, a.x), fma(-R, t.y, a.y));
+      a = na;
+      b = nb;
+    }
   } else {
     double u, v;
     if constexpr (r <= 4) {
@@ -151,7 +159,7 @@ __device__ __forceinline__ void bfly(double2 &a, double2 &b) {
       u = fma(ct, b.x, -b.y);
       v = fma(ct, b.y, b.x);
     }
-    constexpr double f = (r <= 4) ? C32::c[r] : C32::c[8 - r];
+    const double f = ((r <= 4) ? C32::c[r] : C32::c[8 - r]) * R;  // folded at compile time
     double U, V;  // (u + i v) * i^q
     if constexpr (q == 0) { U = u; V = v; }
     else if constexpr (q == 1) { U = -v; V = u; }
@@ -188,6 +196,103 @@ __device__ __forceinline__ void dit32_stage(double2 (&y)[32]) {
 
 __host__ __device__ constexpr int bitrev5(int r) {
   return ((r & 1) << 4) | ((r & 2) << 2) | (r & 4) | ((r & 8) >> 2) | ((r & 16) >> 4);
+}
+
+#ifndef SZ_TAN_TWIST
+#define SZ_TAN_TWIST 0  // measured slower (fwd -4.5 %, inv -8 %: I-cache misses): bit 0: forward, bit 1: inverse (fused with the rounding); negacyclic w^{32m} twist as 2 FMAs (tangent form), scale folded into the DFT / rounding
+#endif
+// cos(pi k / 64), tan(pi k / 64), k = 0..16 (correctly rounded doubles)
+struct C64 {
+  static constexpr double c[17] = {
+      1.0, 0.9987954562051724, 0.9951847266721969, 0.989176509964781, 0.9807852804032304, 0.970031253194544,
+      0.9569403357322088, 0.9415440651830208, 0.9238795325112867, 0.9039892931234433, 0.881921264348355,
+      0.8577286100002721, 0.8314696123025452, 0.8032075314806449, 0.773010453362737, 0.7409511253549591,
+      0.7071067811865476};
+  static constexpr double t[17] = {
+      0.0, 0.049126849769467254, 0.09849140335716425, 0.14833598753834742, 0.198912367379658,
+      0.25048696019130545, 0.3033466836073424, 0.3578057213145241, 0.41421356237309503, 0.4729647758913199,
+      0.5345111359507917, 0.5993769336819238, 0.6681786379192989, 0.7416505462720354, 0.8206787908286604,
+      0.9063471690191471, 1.0};
+};
+// w^{32m} = e^{i th}, th = pi m / 64 < pi/2, written as  s_m * (unscaled factor):
+//   m <= 16: cos th (1 + i tan th)      m > 16: sin th (cot th + i)
+// s_m = twist_scale(m); the unscaled product costs 2 FMAs instead of a 4-op complex multiply.
+__host__ __device__ constexpr double twist_scale(int m) { return m <= 16 ? C64::c[m] : C64::c[32 - m]; }
+template <int M, bool INV>
+__device__ __forceinline__ double2 twist_unscaled(double2 a) {
+  if constexpr (M == 0) {
+    return a;
+  } else if constexpr (M <= 16) {
+    constexpr double t = C64::t[M];
+    return INV ? make_double2(fma(t, a.y, a.x), fma(-t, a.x, a.y)) : make_double2(fma(-t, a.y, a.x), fma(t, a.x, a.y));
+  } else {
+    constexpr double ct = C64::t[32 - M];
+    return INV ? make_double2(fma(ct, a.x, a.y), fma(ct, a.y, -a.x)) : make_double2(fma(ct, a.x, -a.y), fma(ct, a.y, a.x));
+  }
+}
+template <bool INV, int M>
+__device__ __forceinline__ void twist_all_unscaled(double2 (&x)[32]) {
+  if constexpr (M < 32) {
+    x[M] = twist_unscaled<M, INV>(x[M]);
+    twist_all_unscaled<INV, M + 1>(x);
+  }
+}
+
+// DIT stages on inputs that carry pending scales (the factored-out twist
+// scales): before stage H the value at bit-reversed position e carries
+// s(bitrev5(e & ~(H-1))). Butterfly (B+J, B+J+H) computes a + (s_b/s_a) W b,
+// a - (s_b/s_a) W b and both keep s_a; the ratio folds into the butterfly's
+// FMA constants (no extra instructions), and after the last stage every output
+// carries s(bitrev5(0)) = 1.
+template <bool INV, int H, int B, int J>
+__device__ __forceinline__ void dits_bf(double2 (&y)[32]) {
+  if constexpr (B < 32) {
+    if constexpr (J < H) {
+      constexpr double R = twist_scale(bitrev5(B + H)) / twist_scale(bitrev5(B));
+      bfly<J * (16 / H), INV>(y[B + J], y[B + J + H], R);
+      dits_bf<INV, H, B, J + 1>(y);
+    } else {
+      dits_bf<INV, H, B + 2 * H, 0>(y);
+    }
+  }
+}
+template <bool INV, int H>
+__device__ __forceinline__ void dits_stage(double2 (&y)[32]) {
+  if constexpr (H <= 16) {
+    dits_bf<INV, H, 0, 0>(y);
+    dits_stage<INV, 2 * H>(y);
+  }
+}
+// X[k] = sum_m s_m x[m] e^{+-2 pi i m k / 32} for inputs x[m] = (true value) / s_m
+template <bool INV>
+__device__ __forceinline__ void dft32_scaled(double2 (&x)[32]) {
+  double2 y[32];
+#pragma unroll
+  for (int r = 0; r < 32; r++) y[r] = x[bitrev5(r)];
+  dits_stage<INV, 1>(y);
+#pragma unroll
+  for (int r = 0; r < 32; r++) x[r] = y[r];
+}
+
+// inverse untwist of output m fused with the exact rounding of the limb:
+// bits(s_m * u + 1.5 * 2^52) = round(x conj(w^{32m})) + bits(1.5 * 2^52), |.| < 2^51
+template <int M>
+__device__ __forceinline__ void untwist_round_t(double2 y, u64 &bx, u64 &by) {
+  const double2 u = twist_unscaled<M, true>(y);
+  constexpr double s = twist_scale(M);
+  bx = (u64)__double_as_longlong(fma(u.x, s, 6755399441055744.0));
+  by = (u64)__double_as_longlong(fma(u.y, s, 6755399441055744.0));
+}
+__device__ __forceinline__ void untwist_round(double2 y, int m, u64 &bx, u64 &by) {
+  switch (m & 31) {
+#define SZ_U(k) \
+  case k: untwist_round_t<k>(y, bx, by); break;
+    SZ_U(0) SZ_U(1) SZ_U(2) SZ_U(3) SZ_U(4) SZ_U(5) SZ_U(6) SZ_U(7)
+    SZ_U(8) SZ_U(9) SZ_U(10) SZ_U(11) SZ_U(12) SZ_U(13) SZ_U(14) SZ_U(15)
+    SZ_U(16) SZ_U(17) SZ_U(18) SZ_U(19) SZ_U(20) SZ_U(21) SZ_U(22) SZ_U(23)
+    SZ_U(24) SZ_U(25) SZ_U(26) SZ_U(27) SZ_U(28) SZ_U(29) SZ_U(30) SZ_U(31)
+#undef SZ_U
+  }
 }
 
 // 32-point DFT on registers, exponent sign + (conjugate when INV), natural-order
@@ -291,9 +396,14 @@ __device__ __forceinline__ double2 tw_inv(const double2 *sm, int l, int k1) {  /
 // Forward transform of one warp. In: x[m] = (a_j + i a_{j+1024}) at j = lane + 32 m.
 // Out: x[k2] = spectrum at index lane + 32 k2 ("slot" order). `tsm` = shared twiddle copy (SZ_TW_SMEM).
 __device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, const double2 *tsm, int lane) {
+#if SZ_TAN_TWIST & 1
+  twist_all_unscaled<false, 1>(x);
+  dft32_scaled<false>(x);  // x[k1] = B[l = lane][k1]
+#else
 #pragma unroll
   for (int m = 1; m < 32; m++) x[m] = cmul(x[m], c_twist32[m]);
   dft32<false>(x);  // x[k1] = B[l = lane][k1]
+#endif
   __syncwarp();     // earlier readers of buf are done
 #pragma unroll
   for (int k1 = 0; k1 < 32; k1++) buf[sw(lane, k1)] = cmul(x[k1], tw_fwd(tsm, lane, k1));
@@ -303,7 +413,9 @@ __device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, const 
   dft32<false>(x);                                        // x[k2] = Z[lane + 32 k2]
 }
 
-// Inverse transform (unnormalised). In: slot order. Out: x[m] = M (c_j + i c_{j+1024}), j = lane + 32 m.
+// Inverse transform (unnormalised). In: slot order. Out: x[m] = M (c_j + i c_{j+1024}), j = lane + 32 m;
+// with UNTWIST = false the final conj(w^{32m}) is left to the caller (untwist_round).
+template <bool UNTWIST = true>
 __device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, const double2 *tsm, int lane) {
   dft32<true>(x);  // x[l] = 32 B'[l][k1 = lane]
   __syncwarp();
@@ -321,8 +433,10 @@ __device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, const 
   for (int k1 = 0; k1 < 32; k1++) x[k1] = buf[sw(lane, k1)];  // thread l = lane, natural k1
 #endif
   dft32<true>(x);  // x[m] = M z_{lane + 32 m} w^{32 m}
+  if constexpr (UNTWIST) {
 #pragma unroll
-  for (int m = 1; m < 32; m++) x[m] = cmulc(x[m], c_twist32[m]);
+    for (int m = 1; m < 32; m++) x[m] = cmulc(x[m], c_twist32[m]);
+  }
 }
 
 // ------------------------------------------------------------ mbarrier / bulk copy
@@ -606,7 +720,8 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
             else if (i + 1 < n) issue(i + 1, P - 1);
           }
         }
-        inv_fft32(y, xbuf, tsm, lane);
+        constexpr bool kFusedUntwist = (SZ_TAN_TWIST & 2) && SZ_ACC_FAST == 2 && P == 3;
+        inv_fft32<!kFusedUntwist>(y, xbuf, tsm, lane);
         // sum_p bits(M) << p w, removed once per CMux (SZ_ACC_FAST == 2)
         const u64 limb_off = (p == 0) ? kMagicBits + (kMagicBits << w) + (kMagicBits << (2 * w)) : 0ull;
 #if SZ_PUB_FUSED
@@ -618,7 +733,12 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
           acc_ld(ta_acc, cc, a4);
 #pragma unroll
           for (int q = 0; q < kCQ; q++) {
-            if (SZ_ACC_FAST == 2 && P == 3) {
+            if (kFusedUntwist) {
+              u64 bx, by;
+              untwist_round(y[kCQ * cc + q], kCQ * cc + q, bx, by);
+              a4[q][0] += (bx << (p * w)) - limb_off;
+              a4[q][1] += (by << (p * w)) - limb_off;
+            } else if (SZ_ACC_FAST == 2 && P == 3) {
               // branch-free: bits(x + M) << 22p, the magic constant's share removed at p = 0
               a4[q][0] += (limb_bits(y[kCQ * cc + q].x) << (p * w)) - limb_off;
               a4[q][1] += (limb_bits(y[kCQ * cc + q].y) << (p * w)) - limb_off;
