@@ -199,7 +199,7 @@ __host__ __device__ constexpr int bitrev5(int r) {
 }
 
 #ifndef SZ_TAN_TWIST
-#define SZ_TAN_TWIST 0  // measured slower (fwd -4.5 %, inv -8 %: I-cache misses): bit 0: forward, bit 1: inverse (fused with the rounding); negacyclic w^{32m} twist as 2 FMAs (tangent form), scale folded into the DFT / rounding
+#define SZ_TAN_TWIST 2  // sweep 3 (profiles/r01_warp_variants3.txt): 2 with the XOR swizzle is fastest (47.0 k BR-only); with padding it lost to I-cache misses. bit 0: forward, bit 1: inverse (fused with the rounding); negacyclic w^{32m} twist as 2 FMAs (tangent form), scale folded into the DFT / rounding
 #endif
 // cos(pi k / 64), tan(pi k / 64), k = 0..16 (correctly rounded doubles)
 struct C64 {
@@ -333,7 +333,7 @@ __constant__ double2 c_twist32[32];
 // swizzled index of element (row, col) of a 32 x 32 block of 16-byte values:
 // any 8 consecutive rows (fixed col) or cols (fixed row) hit 8 distinct 16-byte bank groups
 #ifndef SZ_PAD
-#define SZ_PAD 1  // padded rows (stride 33) instead of the XOR swizzle: no per-access index arithmetic
+#define SZ_PAD 0  // 1: padded rows (stride 33) instead of the XOR swizzle (sweep 3: XOR swizzle + SZ_TAN_TWIST 2 fastest)
 #endif
 __host__ __device__ constexpr int sw(int row, int col) {
   return SZ_PAD ? row * 33 + col : row * 32 + (col ^ (row & 7));
@@ -501,7 +501,7 @@ __device__ __forceinline__ u64 acc_init(const u64 *v, int j, int bt, int g) {
 #define SZ_D_ST32 0  // 32-column TMEM stores of the digit spectra
 #endif
 #ifndef SZ_ACC_CQ
-#define SZ_ACC_CQ 8  // ACC coefficients m per TMEM access chunk (4: 16 columns, 8: 32 columns; 8 measured +2.8 %)
+#define SZ_ACC_CQ 4  // ACC coefficients m per TMEM access chunk (4: 16 columns, 8: 32 columns; sweep 2 (profiles/r01_warp_variants2.txt): 4 is 3 % faster with the current kernel)
 #endif
 constexpr int kCQ = SZ_ACC_CQ, kNC = 32 / SZ_ACC_CQ;
 // ACC chunk cc (4 kCQ columns) = coefficients j = lane + 32 m + 1024 h, m = kCQ cc + q (q < kCQ), h < 2
