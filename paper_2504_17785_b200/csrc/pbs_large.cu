@@ -15,6 +15,8 @@
 #include <mutex>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "fft.cuh"
 #include "tmem.cuh"
 
@@ -787,6 +789,234 @@ __global__ void __launch_bounds__(256) bsk_to_fourier_huge_kernel(B2FHArgs A) {
   }
 }
 
+// ---------------------------------------------------------------------
+// N = 32768 on a thread-block cluster: the four CTAs of a cluster are the
+// four radix-4 blocks q of one ciphertext (M = 4 x 4096, same transform and
+// tables as blind_rotate_huge_kernel, so the arithmetic is identical), and the
+// per-ciphertext state stays on chip:
+//  * ACC is split by fold position: CTA s owns positions pp in [1024 s, 1024 s
+//    + 1024) of every block mp and both fold halves h (coefficient j = h 16384
+//    + mp 4096 + pp), [comp][h][mp][1024] u64 = 128 KiB of shared memory;
+//  * block q's four digit spectra live in CTA q's tensor memory (as set C);
+//  * the radix-4 steps are all-to-all exchanges through distributed shared
+//    memory: forward, CTA s computes the block inputs x_q[pp] of its positions
+//    from the rotated ACC (remote reads) and stores them into CTA q's FFT
+//    buffer; inverse, CTA q stores its block output at pp into the owner of pp,
+//    which combines the four blocks, rounds and updates its ACC slice.
+// Cluster barriers order the exchanges (two per forward row and per (o, p)).
+#ifndef SZ_SETB_CLUSTER
+#define SZ_SETB_CLUSTER 1  // 0: the global-memory blind_rotate_huge_kernel for every set-B shape
+#endif
+constexpr int kClQ = 4;  // CTAs per ciphertext = radix-4 blocks
+__host__ __device__ constexpr size_t brc_acc_bytes() { return 2 * 2 * 4 * 1024 * sizeof(u64); }
+__host__ __device__ constexpr size_t brc_smem_bytes(int n) {
+  return brc_acc_bytes() + kML * sizeof(double2) + ((size_t)n * 2 + 15) / 16 * 16;
+}
+__device__ __forceinline__ int brc_aidx(int comp, int h, int mp, int loc) { return ((comp * 2 + h) * 4 + mp) * 1024 + loc; }
+
+template <int L, int P>
+__global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rotate_cluster_kernel(BRHArgs A) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  constexpr int rows = 2 * L;
+  static_assert(rows <= 4, "digit spectra must fit tensor memory");
+  u64 *acc = reinterpret_cast<u64 *>(smem);                          // [2][2][4][1024]
+  double2 *buf = reinterpret_cast<double2 *>(smem + brc_acc_bytes()); // [4096] FFT / exchange buffer
+  unsigned short *abar = reinterpret_cast<unsigned short *>(buf + kML);
+  const int t = threadIdx.x, wid = t >> 5;
+  const int q = (int)cl.block_rank();
+  const int n = A.n, w = A.w, blog = A.base_log;
+  // remote (distributed shared memory) addresses: one mapa per access
+#if SZ_DBG_LOCAL
+  auto racc = [&](int rank, int idx) -> const u64 & { (void)rank; return acc[idx]; };
+  auto rbuf = [&](int rank, int idx) -> double2 & { (void)rank; return buf[idx]; };
+#else
+  auto racc = [&](int rank, int idx) -> const u64 & { return *cl.map_shared_rank(acc + idx, rank); };
+  auto rbuf = [&](int rank, int idx) -> double2 & { return *cl.map_shared_rank(buf + idx, rank); };
+#endif
+  __shared__ uint32_t tmem_slot;
+  if (wid == 0) tmem_alloc(&tmem_slot, 512);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t ta_spec = tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16) + 256 * (wid >> 2);
+  const long ncl = gridDim.x / kClQ;
+  for (long c = blockIdx.x / kClQ; c < A.count; c += ncl) {
+    const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
+    for (int i = t; i < n; i += 256) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2NH);
+    const int bt = (int)sz_modswitch(lwe[n], kLog2_2NH);
+    u32 id = A.lut_ids ? A.lut_ids[c] : 0u;
+    if (id >= A.num_luts) id = 0;
+    const u64 *v = A.luts + (size_t)id * kNH;
+    // ACC = (0, X^{-b~} v) on the owned positions
+    for (int e = t; e < 2 * 4 * 1024; e += 256) {
+      const int loc = e & 1023, mp = (e >> 10) & 3, h = e >> 12;
+      const int j = h * kMH + mp * 4096 + 1024 * q + loc;
+      const int idx = (j + bt) & (2 * kNH - 1);
+      acc[brc_aidx(0, h, mp, loc)] = 0;
+      acc[brc_aidx(1, h, mp, loc)] = (idx < kNH) ? v[idx] : (u64)0 - v[idx - kNH];
+    }
+    __syncthreads();
+    for (int i = 0; i < n; i++) {
+      const int a = abar[i];
+      // -------- forward: (r, lvl) digit polynomial -> radix-4 inputs -> block FFT
+#pragma unroll 1
+      for (int r = 0; r < 2; r++) {
+#pragma unroll 1
+        for (int lvl = 1; lvl <= L; lvl++) {
+          cl.sync();  // every buffer is free, every ACC update of the previous CMux is done
+#pragma unroll 1
+          for (int mm = 0; mm < 4; mm++) {
+            const int loc = t + 256 * mm, pp = 1024 * q + loc;
+            double2 vv[4];
+#pragma unroll
+            for (int mp = 0; mp < 4; mp++) {
+              double dv[2];
+#pragma unroll
+              for (int h = 0; h < 2; h++) {
+                const int j = h * kMH + mp * 4096 + pp;
+                const int src = (j - a) & (2 * kNH - 1);
+                const int sj = src & (kNH - 1);
+                const int spp = sj & 4095;
+                const u64 rv = racc(spp >> 10, brc_aidx(r, sj >> 14, (sj >> 12) & 3, spp & 1023));
+                const u64 rot = (src < kNH) ? rv : (u64)0 - rv;
+                u64 rr = sz_decomp_round(rot - acc[brc_aidx(r, h, mp, loc)], blog, L);
+                i64 d = 0;
+#pragma unroll
+                for (int tt = L; tt >= 1; tt--) {
+                  const i64 dd = sz_decomp_next(rr, blog);
+                  if (tt == lvl) d = dd;
+                }
+                dv[h] = (double)d;
+              }
+              vv[mp] = make_double2(dv[0], dv[1]);
+            }
+#pragma unroll
+            for (int qq = 0; qq < 4; qq++) {
+              double2 sacc = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int mp = 0; mp < 4; mp++) sacc = cadd(sacc, cmul(vv[mp], c_CH[mp * 4 + qq]));
+              rbuf(qq, pp) = cmul(sacc, g_FH[qq * 4096 + pp]);
+            }
+          }
+          cl.sync();  // block inputs delivered
+          double2 x[16];
+#pragma unroll
+          for (int m = 0; m < 16; m++) x[m] = buf[t + 256 * m];
+          fwd_fft_L(x, buf, t);
+          const int row = r * L + (lvl - 1);
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) {
+            uint32_t r16[16];
+            pack4(&x[4 * jj], r16);
+            tmem_st16(ta_spec + 64 * row + 16 * jj, r16);
+          }
+        }
+      }
+      tmem_wait_st();
+      // -------- inverse: per output o and limb p: MAC, block IFFT, exchange, combine
+#pragma unroll 1
+      for (int o = 0; o < 2; o++) {
+#pragma unroll 1
+        for (int p = P - 1; p >= 0; p--) {
+          double2 y[16];
+#pragma unroll
+          for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
+#pragma unroll 1
+          for (int row = 0; row < rows; row++) {
+            const double2 *G = A.fbsk + (((((size_t)i * 2 + o) * rows + row) * P + p) * 4 + q) * kML + t;
+#pragma unroll
+            for (int qq = 0; qq < 4; qq += 2) {
+              double2 g[8];
+#pragma unroll
+              for (int k = 0; k < 8; k++) g[k] = __ldg(&G[(4 * qq + k) * 256]);
+              uint32_t d0[16], d1[16];
+              tmem_ld16(ta_spec + 64 * row + 16 * qq, d0);
+              tmem_ld16(ta_spec + 64 * row + 16 * (qq + 1), d1);
+              tmem_wait_ld16x2(d0, d1);
+#pragma unroll
+              for (int k = 0; k < 4; k++) {
+                cmac(y[4 * qq + k], unpack1(d0, k), g[k]);
+                cmac(y[4 * qq + 4 + k], unpack1(d1, k), g[4 + k]);
+              }
+            }
+          }
+          inv_fft_L(y, buf, t);
+          cl.sync();  // every block IFFT is done with its buffer
+#pragma unroll
+          for (int m = 0; m < 16; m++) {
+            const int pp = t + 256 * m;
+            rbuf(pp >> 10, q * 1024 + (pp & 1023)) = y[m];
+          }
+          cl.sync();  // block outputs delivered to the owners
+#pragma unroll 1
+          for (int mm = 0; mm < 4; mm++) {
+            const int loc = t + 256 * mm, pp = 1024 * q + loc;
+            double2 u[4];
+#pragma unroll
+            for (int qq = 0; qq < 4; qq++) u[qq] = cmulc(buf[qq * 1024 + loc], g_FH[qq * 4096 + pp]);
+#pragma unroll
+            for (int mp = 0; mp < 4; mp++) {
+              double2 sacc = make_double2(0.0, 0.0);
+#pragma unroll
+              for (int qq = 0; qq < 4; qq++) sacc = cadd(sacc, cmulc(u[qq], c_CH[mp * 4 + qq]));
+              acc[brc_aidx(o, 0, mp, loc)] += limb_to_torus_L(sacc.x, p, P, w);
+              acc[brc_aidx(o, 1, mp, loc)] += limb_to_torus_L(sacc.y, p, P, w);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    // ---- sample extraction of the owned coefficients: a'[0] = A[0], a'[i] = -A[N-i], b' = B[0]
+    u64 *out = A.lwe_out + (size_t)c * (kNH + 1);
+    for (int e = t; e < 2 * 4 * 1024; e += 256) {
+      const int loc = e & 1023, mp = (e >> 10) & 3, h = e >> 12;
+      const int j = h * kMH + mp * 4096 + 1024 * q + loc;
+      const u64 a0 = acc[brc_aidx(0, h, mp, loc)];
+      if (j == 0) {
+        out[0] = a0;
+        out[kNH] = acc[brc_aidx(1, h, mp, loc)];
+      } else {
+        out[kNH - j] = (u64)0 - a0;
+      }
+    }
+    __syncthreads();
+  }
+  cl.sync();  // no CTA leaves while its shared memory may still be accessed
+  tmem_fence_before();
+  __syncthreads();
+  if (wid == 0) tmem_dealloc(tmem_slot, 512);
+}
+
+static bool cluster_path(const silenzio_params *P) {
+  return SZ_SETB_CLUSTER && P->pbs_level <= 2 && P->fft_limbs == 3 && brc_smem_bytes((int)P->lwe_dim) <= 227 * 1024;
+}
+
+static long cluster_grid(const silenzio_params *P, void (*kern)(BRHArgs), size_t smem) {
+  static long cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
+  if (cached[dev] > 0) return cached[dev];
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kClQ * 64, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = kClQ;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  int ncl = 0;
+  if (cudaOccupancyMaxActiveClusters(&ncl, (void *)kern, &cfg) != cudaSuccess || ncl <= 0) return -1;
+  (void)P;
+  cached[dev] = ncl;
+  return ncl;
+}
+
 size_t blind_rotate_huge_ws_bytes(const silenzio_params *P, size_t count) {
   const long cap = huge_inflight();
   const long inflight = (long)count < cap ? (long)count : cap;
@@ -794,7 +1024,7 @@ size_t blind_rotate_huge_ws_bytes(const silenzio_params *P, size_t count) {
 }
 
 long blind_rotate_huge_wave(const silenzio_params *P) {
-  (void)P;
+  if (cluster_path(P)) return 1L << 40;  // one persistent launch for any count
   return huge_inflight();
 }
 
@@ -803,7 +1033,6 @@ int launch_blind_rotate_huge(const u64 *lwe_small, const u32 *lut_ids, const u64
                              void *workspace, cudaStream_t stream) {
   int st = ensure_tables_huge();
   if (st) return st;
-  if (!workspace) return SILENZIO_ERR_WORKSPACE;
   BRHArgs A;
   A.lwe_small = lwe_small;
   A.lut_ids = lut_ids;
@@ -815,6 +1044,19 @@ int launch_blind_rotate_huge(const u64 *lwe_small, const u32 *lut_ids, const u64
   A.base_log = (int)P->pbs_base_log;
   A.w = (int)P->limb_bits;
   A.ws = reinterpret_cast<unsigned char *>(workspace);
+  A.count = (long)count;
+  if (cluster_path(P)) {
+    void (*ck)(BRHArgs) = P->pbs_level == 2 ? blind_rotate_cluster_kernel<2, 3> : blind_rotate_cluster_kernel<1, 3>;
+    const size_t csmem = brc_smem_bytes(A.n);
+    SZ_CUDA_OK(cudaFuncSetAttribute(ck, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+    const long ncl = cluster_grid(P, ck, csmem);
+    if (ncl <= 0) return SILENZIO_ERR_CUDA;
+    const long grid = (long)count < ncl ? (long)count : ncl;
+    ck<<<(unsigned)(grid * kClQ), 256, csmem, stream>>>(A);  // persistent: cluster g takes ciphertexts g, g + grid, ...
+    SZ_LAUNCH_OK();
+    return SILENZIO_OK;
+  }
+  if (!workspace) return SILENZIO_ERR_WORKSPACE;
   void (*kern)(BRHArgs) = nullptr;
   const int L = (int)P->pbs_level, PP = (int)P->fft_limbs;
   if (L == 2 && PP == 3) kern = blind_rotate_huge_kernel<2, 3>;
