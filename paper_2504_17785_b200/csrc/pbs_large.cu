@@ -814,6 +814,41 @@ __host__ __device__ constexpr size_t brc_smem_bytes(int n) {
 }
 __device__ __forceinline__ int brc_aidx(int comp, int h, int mp, int loc) { return ((comp * 2 + h) * 4 + mp) * 1024 + loc; }
 
+#ifndef SZ_SETB_ASYNCX
+#define SZ_SETB_ASYNCX 1  // exchanges by st.async + mbarriers (point-to-point) instead of cluster barriers
+#endif
+// ---- cluster exchange primitives (shared::cluster addresses are 32-bit)
+__device__ __forceinline__ uint32_t cl_mapa(uint32_t saddr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_mbar_init(uint32_t mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
+}
+// arm this CTA's receive barrier for `bytes` of incoming st.async data (one arrival)
+__device__ __forceinline__ void cl_mbar_expect(uint32_t mbar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
+}
+// release-arrive on a barrier of another CTA of the cluster
+__device__ __forceinline__ void cl_mbar_arrive_remote(uint32_t rmbar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rmbar) : "memory");
+}
+__device__ __forceinline__ void cl_mbar_wait_acq(uint32_t mbar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nSZ_CLW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra SZ_CLW_%=;\n}\n" ::"r"(mbar),
+      "r"(parity)
+      : "memory");
+}
+// 16-byte remote store that completes `16` transaction bytes on the receiver's barrier
+__device__ __forceinline__ void cl_st_async(uint32_t raddr, double2 v, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(v.x), "d"(v.y), "r"(rmbar)
+               : "memory");
+}
+
 template <int L, int P>
 __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rotate_cluster_kernel(BRHArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -841,6 +876,29 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
   __syncthreads();
   tmem_fence_after();
   const uint32_t ta_spec = tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16) + 256 * (wid >> 2);
+  // exchange rounds (SZ_SETB_ASYNCX): every round fills each CTA's buffer with
+  // 4 x 16 KiB from the 4 senders. full = this CTA's receive barrier (armed
+  // with 64 KiB per round); freeb = counts the 4 receivers that released their
+  // buffer for the next round (this CTA sends only after all 4 did).
+  __shared__ __align__(8) uint64_t xbar[2];
+  const uint32_t full = smem_u32(&xbar[0]), freeb = smem_u32(&xbar[1]);
+  const uint32_t buf_s = smem_u32(buf);
+  uint32_t xround = 0;
+  auto release_buf = [&]() {  // after a __syncthreads: this CTA is done with its buffer
+    if (t == 0) {
+      cl_mbar_expect(full, 4 * 1024 * sizeof(double2));
+#pragma unroll
+      for (int r = 0; r < kClQ; r++) cl_mbar_arrive_remote(cl_mapa(freeb, r));
+    }
+  };
+  if (SZ_SETB_ASYNCX) {
+    if (t == 0) {
+      cl_mbar_init(full, 1);
+      cl_mbar_init(freeb, kClQ);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cl.sync();
+  }
   const long ncl = gridDim.x / kClQ;
   for (long c = blockIdx.x / kClQ; c < A.count; c += ncl) {
     const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
@@ -865,7 +923,13 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
       for (int r = 0; r < 2; r++) {
 #pragma unroll 1
         for (int lvl = 1; lvl <= L; lvl++) {
-          cl.sync();  // every buffer is free, every ACC update of the previous CMux is done
+          if (SZ_SETB_ASYNCX) {
+            __syncthreads();  // this CTA's previous use of its buffer (FFT / combination) is over
+            release_buf();
+            cl_mbar_wait_acq(freeb, xround & 1);  // all 4 buffers free, all ACC slices final (release/acquire)
+          } else {
+            cl.sync();  // every buffer is free, every ACC update of the previous CMux is done
+          }
 #pragma unroll 1
           for (int mm = 0; mm < 4; mm++) {
             const int loc = t + 256 * mm, pp = 1024 * q + loc;
@@ -897,10 +961,17 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
               double2 sacc = make_double2(0.0, 0.0);
 #pragma unroll
               for (int mp = 0; mp < 4; mp++) sacc = cadd(sacc, cmul(vv[mp], c_CH[mp * 4 + qq]));
-              rbuf(qq, pp) = cmul(sacc, g_FH[qq * 4096 + pp]);
+              const double2 xv = cmul(sacc, g_FH[qq * 4096 + pp]);
+              if (SZ_SETB_ASYNCX) cl_st_async(cl_mapa(buf_s + pp * 16, qq), xv, cl_mapa(full, qq));
+              else rbuf(qq, pp) = xv;
             }
           }
-          cl.sync();  // block inputs delivered
+          if (SZ_SETB_ASYNCX) {
+            cl_mbar_wait_acq(full, xround & 1);  // block inputs delivered
+            xround++;
+          } else {
+            cl.sync();  // block inputs delivered
+          }
           double2 x[16];
 #pragma unroll
           for (int m = 0; m < 16; m++) x[m] = buf[t + 256 * m];
@@ -943,13 +1014,26 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
             }
           }
           inv_fft_L(y, buf, t);
-          cl.sync();  // every block IFFT is done with its buffer
+          if (SZ_SETB_ASYNCX) {
+            __syncthreads();  // this CTA's IFFT is done with its buffer
+            release_buf();
+            cl_mbar_wait_acq(freeb, xround & 1);
 #pragma unroll
-          for (int m = 0; m < 16; m++) {
-            const int pp = t + 256 * m;
-            rbuf(pp >> 10, q * 1024 + (pp & 1023)) = y[m];
+            for (int m = 0; m < 16; m++) {
+              const int pp = t + 256 * m;
+              cl_st_async(cl_mapa(buf_s + (q * 1024 + (pp & 1023)) * 16, pp >> 10), y[m], cl_mapa(full, pp >> 10));
+            }
+            cl_mbar_wait_acq(full, xround & 1);  // block outputs delivered to the owners
+            xround++;
+          } else {
+            cl.sync();  // every block IFFT is done with its buffer
+#pragma unroll
+            for (int m = 0; m < 16; m++) {
+              const int pp = t + 256 * m;
+              rbuf(pp >> 10, q * 1024 + (pp & 1023)) = y[m];
+            }
+            cl.sync();  // block outputs delivered to the owners
           }
-          cl.sync();  // block outputs delivered to the owners
 #pragma unroll 1
           for (int mm = 0; mm < 4; mm++) {
             const int loc = t + 256 * mm, pp = 1024 * q + loc;
