@@ -289,7 +289,10 @@ def main():
                 # dram__bytes_read.sum + dram__bytes_write.sum of one full-wave launch (592 ciphertexts) from
                 # the committed ncu --set full capture (151.5 MB read = the 146 MB Fourier BSK once per wave
                 # + inputs; 6.1 MB written): per launch, HBM is far from the bound
-                "traffic": 157.6e6, "traffic_source": "profiles/r01_ncu_blind_rotate_warp.txt (per launch)",
+                "traffic": 1.868252e12,
+                "traffic_source": "profiles/r01_ncu_br_bench_dram.txt: dram__bytes_read.sum + dram__bytes_write.sum "
+                                  "of the bench's 131072-ciphertext launch (the drifting persistent grid re-reads the "
+                                  "146 MB Fourier BSK; HBM stays at ~10 % of its bandwidth, see DESIGN.md §6)",
                 "kernel": "blind_rotate_warp_kernel<3>", "algorithmic_flops_per_pbs": flops,
                 "kernel_ms": float(np.mean(br_ms)), "keyswitch_ms": float(np.mean(ks_ms)),
                 "peak_source": "measured DFMA burst (tools/microbench/mb.cu, profiles/r01_microbench_b200.txt)",

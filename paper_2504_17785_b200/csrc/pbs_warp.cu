@@ -539,6 +539,16 @@ __device__ __forceinline__ u64 limb_bits(double x) { return (u64)__double_as_lon
 constexpr u64 kMagicBits = 0x4338000000000000ull;  // bits of 1.5 * 2^52
 constexpr u64 kLimbOffset3 = kMagicBits + (kMagicBits << 22) + (kMagicBits << 44);  // sum_p bits(M) << 22 p
 
+#ifndef SZ_ROUND_SYNC
+#define SZ_ROUND_SYNC 0  // W > 0: a CTA starts round r only after every CTA finished round r - W. Measured at 131 072
+                         // (tools/ab_roundsync.sh): W = 1 cuts DRAM reads 56x (1.87 TB -> 34 GB per launch) but is
+                         // 28 % slower (all CTAs hammer the same BSK lines in L2); W = 2: 1.8x fewer reads, 14 % slower.
+                         // The drifting persistent grid is FP64-bound with HBM at ~10 % of its bandwidth, so 0.
+#endif
+#if SZ_ROUND_SYNC
+__device__ unsigned int g_round_done;
+#endif
+
 template <int P>
 __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -575,7 +585,22 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   if (tid == 0) mac_done = 0;
 
   const long ngroups = (A.count + kCts - 1) / kCts;
-  for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  long round_no = 0;
+  for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x, round_no++) {
+#if SZ_ROUND_SYNC
+    if (round_no >= SZ_ROUND_SYNC) {
+      if (tid == 0) {
+        const unsigned need = (unsigned)((round_no - SZ_ROUND_SYNC + 1) * gridDim.x);
+        unsigned v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&g_round_done) : "memory");
+          if (v >= need) break;
+          __nanosleep(256);
+        }
+      }
+      __syncthreads();
+    }
+#endif
     if (tid == 0) issue(0, P - 1);
     const long c_raw = grp * kCts + cs;
     const bool live = c_raw < A.count;
@@ -796,6 +821,9 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
       }
     }
     __syncthreads();  // abar reuse
+#if SZ_ROUND_SYNC
+    if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&g_round_done) : "memory");
+#endif
   }
   tmem_fence_before();
   __syncthreads();
@@ -892,6 +920,13 @@ int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64
     // over one launch per resident wave (which kept every CTA on the same BSK_i)
     const long groups = ((long)count + w32::kCts - 1) / w32::kCts;
     const long grid = groups < wave / w32::kCts ? groups : wave / w32::kCts;
+#if SZ_ROUND_SYNC
+    {
+      void *ctr = nullptr;
+      SZ_CUDA_OK(cudaGetSymbolAddress(&ctr, w32::g_round_done));
+      SZ_CUDA_OK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream));
+    }
+#endif
     kern<<<(unsigned)grid, w32::kThreads, smem, stream>>>(A);
     SZ_LAUNCH_OK();
     return SILENZIO_OK;

@@ -58,6 +58,25 @@ def test_setb_trivial_identity_bitexact(dev):
     assert np.array_equal(out[:, -1], np.array([T[m] if m < 256 else negT[m - 256] for m in ms], dtype=np.uint64))
 
 
+def test_setb_trivial_identity_persistent_clusters_bitexact(dev):
+    """More ciphertexts than co-resident 4-CTA clusters (each cluster loops over
+    several ciphertexts): the trivial identity must hold bit-exactly for all."""
+    from paper_2504_17785_b200 import workload as wl
+    P, ok, gk = setup("B_SMALLN", 5, dev)
+    tab = np.array([[(7 * x + 3) % 256 for x in range(256)], [(x * x + 1) % 256 for x in range(256)]])
+    lut = wl.luts_from_tables(tab, P.p, P.N, dev)
+    T = oracle.encode(tab, P.p)
+    cnt = 150
+    ms = np.arange(cnt) * 37 % 512
+    ids = np.arange(cnt) % 2
+    small = np.zeros((cnt, P.n + 1), dtype=np.uint64)
+    small[:, -1] = oracle.encode(ms, P.p)
+    out = br(P, gk, small, lut, dev, ids=ids)
+    assert (out[:, :-1] == 0).all()
+    want = np.array([T[l, m] if m < 256 else (~T[l, m - 256]) + np.uint64(1) for l, m in zip(ids, ms)], dtype=np.uint64)
+    assert np.array_equal(out[:, -1], want)
+
+
 def test_setb_exact_gadget_bitexact(dev):
     from paper_2504_17785_b200 import workload as wl
     P, ok, gk = setup("EXACT32768", 3, dev)
