@@ -200,3 +200,74 @@ def int_ce_loss_deriv(Yhat, Y, gamma: int, kappa: int):
     E = round_half_even((E * 2 ** kappa + 1) / (S + 1))
     E = E - np.asarray(Y, dtype=np.int64) * E.sum(axis=1, keepdims=True)
     return (E > 0).astype(np.int64) - (E < 0).astype(np.int64)
+
+
+# ------------------------------------------------- Alg. 6 end-to-end training
+# one training step of an MLP (Alg. 6,
+# P:466-502) at the 4-bit widths of parameter set A (R23-R26).
+BASES4 = [(13, 16), (11, 13, 16), (9, 11, 13, 16), (7, 9, 11, 13, 16), (5, 7, 9, 11, 13, 16)]
+
+
+def relu_cap(a, x: int):
+    """P:269-274: ReLU_x(a) = min(max(a, 0), x), x >= 0."""
+    return np.minimum(np.maximum(np.asarray(a, dtype=np.int64), 0), x)
+
+
+def get_rns_base(max_abs: int):
+    """getRNSBase over the 4-bit moduli the Matmul^RNS schedule
+    supports, even modulus last (R24): the smallest base whose signed
+    range [-M/2, M/2) holds every value of magnitude <= max_abs."""
+    for base in BASES4:
+        if math.prod(base) > 2 * max_abs + 1:
+            return list(base)
+    raise ValueError("no 4-bit RNS base covers the range")
+
+
+def matmul_bound(b: int, max_x: int, max_w: int) -> int:
+    """max |X W| for X in [-max_x, max_x]^{a x b}, W in [-max_w, max_w]^{b x c}."""
+    return b * max_x * max_w
+
+
+def train_step(A0, Y, Ws, Gamma: int = 4, w: int = 4, cap: int = 7, wmin: int = -8, wmax: int = 7):
+    """Alg. 6 for one batch, every step in the paper's order, with
+    the activations it omits "for brevity" (R25): hidden layers
+    A_l = ReLU_x(Shift2MSBs+-(A_{l-1} W_l^T)), the output layer keeps the
+    Shift2MSBs+- logits; the propagated error is Sign^RNS_(-1,0,1)(E W_l) times
+    the ReLU_x derivative [0 < S_{l-1} < x]; weights W_l <- clip(W_l - G_l)
+    with G_l = Sign^RNS_(-1,0,1)(E^T A_{l-1}). Matmuls and signs run on the
+    RNS residues (Alg. 2, Sign^RNS P:309-323) in the base getRNSBase picks, so
+    every intermediate equals what the encrypted schedule must decrypt to.
+    A0 [a][b_1] in [-8, 8), Y [a][c_L] one-hot, Ws[l] [c_l][b_l] in [wmin, wmax].
+    Returns the new weights and every intermediate."""
+    A0 = np.asarray(A0, dtype=np.int64)
+    L = len(Ws)
+    acts, pre, bases_f, Z = [A0], [], [], []
+    # ---- forward pass
+    for l in range(L):
+        W = np.asarray(Ws[l], dtype=np.int64)
+        Ain = acts[-1]
+        base = get_rns_base(matmul_bound(W.shape[1], 8, 8))
+        res = matmul_rns(Ain, W.T, base)                   # k x a x c_l residues
+        S, _ = shift2msbs_pm(res, base, w, Gamma)         # Gamma-bit signed
+        bases_f.append(base)
+        Z.append(signed_decode(crt(res, base), math.prod(base)))
+        pre.append(S)
+        acts.append(relu_cap(S, cap) if l < L - 1 else S)
+    # ---- backward pass
+    E = int_ce_loss_deriv(acts[-1], Y, Gamma - 1, 0)
+    errs, grads, newW = [E], [None] * L, [None] * L
+    for l in range(L - 1, -1, -1):
+        W = np.asarray(Ws[l], dtype=np.int64)
+        Aprev = acts[l]
+        gbase = get_rns_base(matmul_bound(Aprev.shape[0], 1, 8))
+        G = sign_rns(matmul_rns(E.T, Aprev, gbase), gbase)
+        if l > 0:
+            ebase = get_rns_base(matmul_bound(W.shape[0], 1, 8))
+            En = sign_rns(matmul_rns(E, W, ebase), ebase)
+            S = pre[l - 1]
+            E = En * ((S > 0) & (S < cap)).astype(np.int64)   # ReLU_x derivative (R25)
+            errs.append(E)
+        grads[l] = G
+        newW[l] = np.clip(W - G, wmin, wmax)
+    return newW, {"pre": pre, "acts": acts, "Z": Z, "errs": errs, "grads": grads, "bases": bases_f,
+                  "W_in": [np.asarray(W, dtype=np.int64) for W in Ws]}

@@ -1,0 +1,220 @@
+"""One Silenzio training step (Alg. 6) on encrypted data.
+
+SURVEY.md §8(f) NEXT #1. A host-side schedule over the C ABI: every arithmetic
+step is a libsilenzio kernel launch (PBS, linear LWE combinations, Matmul^RNS,
+RNS2MRNS, the 8-bit digit combine, IntCELossDeriv); this module only builds
+LUT tables, sequences the calls and reshapes ciphertext arrays. There is no
+CPU fallback: without the CUDA library every call raises.
+
+Widths and readings (R23-R26): parameter set A (4-bit messages +
+padding, Delta = 2^59) for every LUT except the 8-bit MRNS digit combine of
+Shift2MSBs+- (set B); alpha = beta = Gamma = 4, ReLU cap x = 7, weights clipped
+to [-8, 7]; getRNSBase over {5, 7, 9, 11, 13} + 16. New 4-bit gadgets here:
+  * channel16: the m = 16 residue Matmul^RNS emits at 2^60 -> Delta (2 PBS),
+  * sign3: Sign^RNS_(-1,0,1): top MRNS digit >= 8 and the zero
+    test (sum of [digit != 0] over the digits) packed into one PBS,
+  * relu_cap, relu_mask (ReLU_x and its derivative times an error sign),
+  * update: clip(W - G) for G in {-1, 0, 1} as two bit x 4-bit products
+    (toolbox T4) plus a refreshing identity PBS.
+The cleartext result every step must decrypt to is oracle.gadgets.train_step
+(tests/test_gpu_training.py)."""
+import math
+
+import numpy as np
+import torch
+
+from . import silenzio as sz
+from . import workload as wl
+
+DLOG = 59            # set A: Delta = 2^59
+W_BITS = 4           # RNS modulus bit width w of Shift2MSBs
+BASES4 = [(13, 16), (11, 13, 16), (9, 11, 13, 16), (7, 9, 11, 13, 16), (5, 7, 9, 11, 13, 16)]
+
+
+def get_rns_base(max_abs: int):
+    """getRNSBase (R24): smallest base with M > 2 max_abs + 1."""
+    for base in BASES4:
+        if math.prod(base) > 2 * max_abs + 1:
+            return list(base)
+    raise ValueError("no 4-bit RNS base covers the range")
+
+
+def _u64(v: int) -> int:
+    return int(v) % (1 << 64)
+
+
+def table16(fn, w0: int, scale_log: int = DLOG) -> np.ndarray:
+    """16 torus values realising fn on the input window [w0, w0 + 16) of Z_32:
+    index x mod 32 < 16 reads T[x mod 32], otherwise -T[x mod 32 - 16]
+    (negacyclic test polynomial). fn(x) is in units of
+    2^scale_log (half-step outputs: scale_log = DLOG - 1)."""
+    tab = [0] * 16
+    for x in range(w0, w0 + 16):
+        xm, v = x % 32, _u64(int(fn(x)) << scale_log)
+        if xm < 16:
+            tab[xm] = v
+        else:
+            tab[xm - 16] = _u64(-v)
+    return np.array(tab, dtype=np.uint64)
+
+
+class Context:
+    """Keys of both parameter sets and the cross-parameter keyswitching keys."""
+
+    def __init__(self, PA, PB, ka, kb, ksk_ab, pab, ksk_ba, pba, device):
+        self.PA, self.PB, self.ka, self.kb = PA, PB, ka, kb
+        self.ksk_ab, self.pab, self.ksk_ba, self.pba = ksk_ab, pab, ksk_ba, pba
+        self.dev = device
+        self.dim = PA.k * PA.N
+        self.pbs_count = 0
+        self._lut_cache = {}
+
+    # ---------------------------------------------------------- primitives
+    def luts(self, tables):
+        key = tuple(t.tobytes() for t in tables)
+        if key not in self._lut_cache:
+            self._lut_cache[key] = sz.build_testpoly(wl.to_dev(np.stack(tables), self.dev), 4, self.PA.N)
+        return self._lut_cache[key]
+
+    def pbs(self, ct, tables, ids=None):
+        """PBS of every row of ct [count][dim+1] with tables[ids[i]]."""
+        ct = ct.reshape(-1, self.dim + 1).contiguous()
+        if ids is not None:
+            ids = torch.as_tensor(np.asarray(ids, np.int32), device=self.dev)
+        self.pbs_count += ct.shape[0]
+        return sz.pbs_batch(ct, ids, self.luts(tables), self.ka["fbsk"], self.ka["ksk"], self.PA)
+
+    def lin(self, terms, cst: int = 0):
+        """sum_t coef_t ct_t + cst (elementwise over rows) by one linear kernel."""
+        cts = [c.reshape(-1, self.dim + 1) for _, c in terms]
+        count = cts[0].shape[0]
+        stacked = torch.cat(cts, 0).contiguous()
+        T = len(terms)
+        idx = (torch.arange(T, dtype=torch.int64, device=self.dev)[None, :] * count
+               + torch.arange(count, dtype=torch.int64, device=self.dev)[:, None]).to(torch.int32)
+        coef = torch.tensor([int(c) for c, _ in terms], dtype=torch.int64, device=self.dev).repeat(count, 1)
+        cst_t = torch.full((count,), np.int64(np.uint64(_u64(cst)).view(np.int64)), dtype=torch.int64,
+                           device=self.dev)
+        return sz.lwe_linear_batch(stacked, idx.contiguous(), coef.contiguous(), cst_t)
+
+    def decrypt(self, ct, signed_mod: int = 32):
+        """Test/diagnostic helper: decode every row (set-A big key)."""
+        ph = wl.to_host_u64(sz.lwe_phase_batch(ct.reshape(-1, self.dim + 1).contiguous(), self.ka["big_key"]))
+        v = wl.decode(ph, 4)
+        return np.where(2 * v >= signed_mod, v - signed_mod, v)
+
+    # ------------------------------------------------------------- gadgets
+    def matmul(self, X, W, base):
+        """Matmul^RNS (Alg. 2) -> residues [k][a][c] all at Delta (channel16 applied)."""
+        res = sz.rns_matmul(X.contiguous(), W.contiguous(), base, self.ka["fbsk"], self.ka["ksk"], self.PA)
+        k, a, c = res.shape[0], res.shape[1], res.shape[2]
+        if base[-1] == 16:
+            res[k - 1] = self.channel16(res[k - 1]).reshape(a, c, -1)
+        return res
+
+    def channel16(self, z):
+        """r at 2^60 (r in [0, 16), the native mod-16 channel) -> r at Delta.
+        z reads index 2r of Z_32; s' = PBS(z; -4) is -4 for r < 8 and +4 for
+        r >= 8 (negacyclic), x = z - 2 s' - 8 = 2 (r mod 8), and
+        r = PBS(x; x/2 + 4) + s' (toolbox T4 with e = [r >= 8])."""
+        sp = self.pbs(z, [table16(lambda x: -4, 0)])
+        x = self.lin([(1, z), (-2, sp)], cst=-8 << DLOG)
+        hi = self.pbs(x, [table16(lambda v: v // 2 + 4, 0)])
+        return self.lin([(1, hi), (1, sp)])
+
+    def shift2msbs(self, res, base):
+        """Shift2MSBs+- (Alg. 4) to Gamma = 4: residues [k][count] -> [count] in [-7, 7]."""
+        ka = self.ka
+        digits = sz.rns2mrns(res, base, ka["fbsk"], ka["ksk"], self.PA)
+        _, absr = sz.rns_sign_abs(res, base, ka["fbsk"], ka["ksk"], self.PA)
+        dabs = sz.rns2mrns(absr, base, ka["fbsk"], ka["ksk"], self.PA)
+        _, mx = sz.mrns_bitlen_max(dabs, ka["fbsk"], ka["ksk"], self.PA)
+        Y, _ = sz.mrns_digit_combine(digits[-1].contiguous(), dabs, mx, base[-1], W_BITS, 3, ka, self.PA,
+                                     self.kb, self.PB, self.ksk_ab, self.pab, self.ksk_ba, self.pba)
+        return Y
+
+    def sign3(self, res, base):
+        """Sign^RNS_(-1,0,1): [count] in {-1, 0, 1} at Delta."""
+        ka = self.ka
+        digits = sz.rns2mrns(res, base, ka["fbsk"], ka["ksk"], self.PA)
+        k = len(base)
+        nz = [self.pbs(digits[i], [table16(lambda v: 1 if v else 0, 0)]) for i in range(k)]
+        top = base[-1] // 2
+        e = self.pbs(digits[k - 1], [table16(lambda v: 8 if v >= top else 0, 0)])
+        packed = self.lin([(1, t) for t in nz] + [(1, e)])        # sum of [d != 0] + 8 [neg], in [0, 14]
+        return self.pbs(packed, [table16(lambda v: 0 if v % 8 == 0 else (-1 if v >= 8 else 1), 0)])
+
+    def relu_cap(self, S, cap: int):
+        return self.pbs(S, [table16(lambda v: min(max(v, 0), cap), -8)])
+
+    def relu_mask(self, E, S, cap: int):
+        """E in {-1, 0, 1} times the ReLU_x derivative [0 < S < cap] (R25)."""
+        m4 = self.pbs(S, [table16(lambda v: 4 if 0 < v < cap else 0, -8)])
+        packed = self.lin([(1, E), (1, m4)], cst=1 << DLOG)      # (E + 1) + 4 [mask], in [0, 6]
+        return self.pbs(packed, [table16(lambda v: v - 5 if v >= 4 else 0, 0)])
+
+    def update(self, W, G, wmin: int = -8, wmax: int = 7):
+        """clip(W - G) for W in [wmin, wmax], G in {-1, 0, 1}:
+        W - G + [W = wmin][G = 1] - [W = wmax][G = -1] written as
+        W - e+ [W != wmin] + e- [W != wmax], each product a bit x 4-bit T4:
+        f(e, W) = PBS(W; (g0 + g1)/2) + PBS(16 e + W; (g0 - g1)/2) (half steps),
+        then a refreshing identity PBS (fresh noise for the next step)."""
+        ep = self.pbs(G, [table16(lambda g: 1 if g == 1 else 0, -8)])
+        em = self.pbs(G, [table16(lambda g: 1 if g == -1 else 0, -8)])
+        h = DLOG - 1
+        A1 = self.pbs(W, [table16(lambda v: -(v != wmin), -8, h)])
+        B1 = self.pbs(self.lin([(16, ep), (1, W)]), [table16(lambda v: (v != wmin), -8, h)])
+        A2 = self.pbs(W, [table16(lambda v: (v != wmax), -8, h)])
+        B2 = self.pbs(self.lin([(16, em), (1, W)]), [table16(lambda v: -(v != wmax), -8, h)])
+        s = self.lin([(1, W), (1, A1), (1, B1), (1, A2), (1, B2)])
+        return self.pbs(s, [table16(lambda v: v, -8)])
+
+    # ------------------------------------------------------- one training step
+    def train_step(self, A0, Y, Ws, cap: int = 7, keep=False):
+        """A0 [a][b_1], Y [a][c_L] one-hot bits, Ws[l] [c_l][b_l] (ciphertexts
+        [..][dim+1] on the device) -> new weights (and intermediates if keep)."""
+        L = len(Ws)
+        a = A0.shape[0]
+        acts, pre, inter = [A0], [], {"pre": [], "acts": [], "errs": [], "grads": []}
+        for l in range(L):
+            W = Ws[l]
+            c_l, b_l = W.shape[0], W.shape[1]
+            base = get_rns_base(b_l * 64)
+            res = self.matmul(acts[-1], W.transpose(0, 1), base)          # [k][a][c_l]
+            S = self.shift2msbs(res.reshape(len(base), a * c_l, -1), base).reshape(a, c_l, -1)
+            pre.append(S)
+            acts.append(self.relu_cap(S, cap).reshape(a, c_l, -1) if l < L - 1 else S)
+        E = sz.int_ce_grad(acts[-1].contiguous(), Y.contiguous(), self.ka["fbsk"], self.ka["ksk"], self.PA)
+        inter["errs"].append(E)
+        newW = [None] * L
+        for l in range(L - 1, -1, -1):
+            W = Ws[l]
+            c_l, b_l = W.shape[0], W.shape[1]
+            gbase = get_rns_base(a * 8)
+            G = self.sign3(self.matmul(E.transpose(0, 1), acts[l], gbase).reshape(len(gbase), c_l * b_l, -1),
+                           gbase).reshape(c_l, b_l, -1)
+            if l > 0:
+                ebase = get_rns_base(c_l * 8)
+                En = self.sign3(self.matmul(E, W, ebase).reshape(len(ebase), a * b_l, -1), ebase)
+                E = self.relu_mask(En, pre[l - 1].reshape(a * b_l, -1), cap).reshape(a, b_l, -1)
+                inter["errs"].append(E)
+            inter["grads"].insert(0, G)
+            newW[l] = self.update(W.reshape(c_l * b_l, -1), G.reshape(c_l * b_l, -1)).reshape(c_l, b_l, -1)
+        inter["pre"], inter["acts"] = pre, acts
+        return (newW, inter) if keep else newW
+
+
+def make_context(PA, PB, seed: int, device, ks_ab=(4, 5), ks_ba=(10, 4)):
+    """Keys from the seeded draws of synth/ (set A, set B, cross KSKs, R8)."""
+    from synth import cross_ksk_randomness, key_randomness
+    ra, rb = key_randomness(PA, seed), key_randomness(PB, seed + 1)
+    ka, kb = wl.device_keys(PA, ra, device), wl.device_keys(PB, rb, device)
+    rab = cross_ksk_randomness(PA.big_dim, ks_ab[1], PB.n, PB.lwe_sigma_log2, seed, 1)
+    rba = cross_ksk_randomness(PB.big_dim, ks_ba[1], PA.big_dim, PA.glwe_sigma_log2, seed, 2)
+    ksk_ab = sz.ksk_generate(ka["big_key"], kb["lwe_key"], wl.to_dev(rab["ksk_mask"], device),
+                             wl.to_dev(rab["ksk_noise"], device), *ks_ab)
+    ksk_ba = sz.ksk_generate(kb["big_key"], ka["big_key"], wl.to_dev(rba["ksk_mask"], device),
+                             wl.to_dev(rba["ksk_noise"], device), *ks_ba)
+    pab = sz.ks_params(PA.big_dim, PB.n, *ks_ab, like=PB)
+    pba = sz.ks_params(PB.big_dim, PA.big_dim, *ks_ba, like=PB)
+    return Context(PA, PB, ka, kb, ksk_ab, pab, ksk_ba, pba, device)

@@ -162,3 +162,43 @@ def test_exact_block_scale_and_shift2msbs_error_statistic():
         assert np.abs(Y).max() <= 7 and np.abs(E).max() <= 7
         print("Shift2MSBs+- vs exact block scaling: exact shift", s, "mean |err|", e.mean(), "max", e.max())
         assert e.mean() <= mean_bound and e.max() <= max_bound
+
+
+# ----------------------------------------------- Alg. 6 training step (NEXT #1)
+def test_train_step_pinned_to_plain_integer_math():
+    """oracle.gadgets.train_step (cleartext Alg. 6, R23-R26) against plain
+    integer numpy: every RNS matmul CRT-decodes to the integer product, the
+    gradient and error signs are np.sign of the plain products (times the
+    ReLU_x derivative), the update is np.clip(W - G), the activations are
+    min(max(S, 0), 7), and getRNSBase picks the smallest sufficient base."""
+    import math
+    rng = np.random.default_rng(7)
+    for dims, batch in (([6, 3, 2], 4), ([28, 8, 2], 8), ([13, 8, 3], 8)):
+        A0 = rng.integers(-8, 8, size=(batch, dims[0]))
+        Ws = [rng.integers(-8, 8, size=(dims[l + 1], dims[l])) for l in range(len(dims) - 1)]
+        Y = np.zeros((batch, dims[-1]), dtype=np.int64)
+        Y[np.arange(batch), rng.integers(0, dims[-1], size=batch)] = 1
+        newW, it = G.train_step(A0, Y, Ws)
+        L = len(Ws)
+        for l in range(L):
+            assert np.array_equal(it["Z"][l], it["acts"][l] @ Ws[l].T)           # Matmul^RNS + CRT
+            S = it["pre"][l]
+            assert S.min() >= -7 and S.max() <= 7                                # Gamma = 4 signed
+            want = np.minimum(np.maximum(S, 0), 7) if l < L - 1 else S
+            assert np.array_equal(it["acts"][l + 1], want)
+        E = it["errs"][0]
+        assert set(np.unique(E)) <= {-1, 0, 1}
+        for l in range(L - 1, -1, -1):
+            Gl = np.sign(E.T @ it["acts"][l])
+            assert np.array_equal(it["grads"][l], Gl)
+            assert np.array_equal(newW[l], np.clip(Ws[l] - Gl, -8, 7))
+            if l > 0:
+                S = it["pre"][l - 1]
+                E = np.sign(E @ Ws[l]) * ((S > 0) & (S < 7))
+                assert np.array_equal(it["errs"][L - l], E)
+    for bound in (1, 50, 103, 104, 1143, 1144, 10295, 10296, 72071, 72072, 360359):
+        base = G.get_rns_base(bound)
+        M = math.prod(base)
+        assert M > 2 * bound + 1 and base[-1] == 16
+        smaller = [b for b in G.BASES4 if math.prod(b) < M]
+        assert all(math.prod(b) <= 2 * bound + 1 for b in smaller)
