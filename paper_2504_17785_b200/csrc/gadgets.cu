@@ -98,12 +98,24 @@ using namespace szg;
 
 extern "C" {
 
+// Rows of X processed per pass: enough products per PBS batch to fill the GPU
+// (a PBS launch costs one full blind rotation of latency whatever its size), at
+// most one row when a single row already gives >= kPassProducts products.
+constexpr size_t kPassProducts = 4096;
+static uint32_t rows_per_pass(uint32_t a, uint32_t b, uint32_t c) {
+  const size_t per_row = (size_t)b * c;
+  size_t r = (kPassProducts + per_row - 1) / per_row;
+  if (r < 1) r = 1;
+  return (uint32_t)(r < a ? r : a);
+}
+
 size_t silenzio_rns_matmul_workspace_bytes(const silenzio_params *P, uint32_t a, uint32_t b, uint32_t c) {
-  if (!P) return 0;
+  if (!P || a == 0) return 0;
   const size_t big = (size_t)P->glwe_dim * P->poly_size + 1;
   const size_t ct = big * 8;
+  const size_t R = rows_per_pass(a, b, c);
   const size_t xr = 2 * (size_t)a * b, wr = 2 * (size_t)b * c;   // residues / digits of one modulus
-  const size_t prod = 4 * (size_t)b * c;                           // per row of X: up to 4 ciphertexts per product
+  const size_t prod = 4 * R * b * c;                               // per pass of R rows: up to 4 ciphertexts per product
   const size_t bufs = xr + wr + 4 * prod;                          // X', W', 4 row buffers
   const size_t idx_cap = 2 * prod;
   const size_t pbs_cap = 65536;
@@ -131,7 +143,8 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
   D.ksk = ksk;
   D.big = (size_t)P->glwe_dim * P->poly_size + 1;
   const size_t ctw = D.big;  // words per ciphertext
-  const size_t xr = 2 * (size_t)a * b, wr = 2 * (size_t)b * c, prod = 4 * (size_t)b * c;
+  const uint32_t RP = rows_per_pass(a, b, c);
+  const size_t xr = 2 * (size_t)a * b, wr = 2 * (size_t)b * c, prod = 4 * (size_t)RP * b * c;
   unsigned char *p = reinterpret_cast<unsigned char *>(workspace);
   auto carve = [&](size_t bytes) {
     unsigned char *r = p;
@@ -180,20 +193,23 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
       std::fill(idsw.begin(), idsw.end(), 1u);
       if ((rc = lookup(D, W, Wr + nW * ctw, nW, idsw, 2))) return rc;
     }
-    // ---------------- per row i of X: products over (j, kk) then the sum tree per j
-    for (uint32_t i = 0; i < a; i++) {
-      // Linear inputs address one array: gather the row of X' and all of W'
-      // as [X'(i, 0..b) | W'(0..b, 0..c)] (digits doubled for m = 16).
+    // ---------------- per pass of R rows i0.. of X: products over (r, j, kk), then
+    // the sum tree per output (r, j)
+    for (uint32_t i0 = 0; i0 < a; i0 += RP) {
+      const uint32_t R = (a - i0 < RP) ? a - i0 : RP;
+      const uint32_t i = i0;
+      // Linear inputs address one array: gather the rows of X' and all of W'
+      // as [X'(i0..i0+R, 0..b) | W'(0..b, 0..c)] (digits doubled for m = 16).
       const size_t xw = (m == 16) ? 2 : 1;
-      const size_t nrow = xw * b, nw = xw * nW;
-      // stage row i of X' (and its digit plane) into T3, W' after it
+      const size_t nrow = xw * R * b, nw = xw * nW;
+      // stage rows i0.. of X' (and their digit plane) into T3, W' after them
       for (size_t d = 0; d < xw; d++)
-        SZ_CUDA_OK(cudaMemcpyAsync(T3 + d * b * ctw, Xr + (d * nX + (size_t)i * b) * ctw, b * ctw * 8,
+        SZ_CUDA_OK(cudaMemcpyAsync(T3 + d * R * b * ctw, Xr + (d * nX + (size_t)i0 * b) * ctw, R * b * ctw * 8,
                                    cudaMemcpyDeviceToDevice, D.st));
       SZ_CUDA_OK(cudaMemcpyAsync(T3 + nrow * ctw, Wr, nw * ctw * 8, cudaMemcpyDeviceToDevice, D.st));
-      // product index e = j * b + kk  (products of one output are contiguous)
-      const size_t np = (size_t)c * b;
-      auto xi = [&](size_t d, size_t kk) { return (u32)(d * b + kk); };
+      // product index e = (r c + j) b + kk  (products of one output are contiguous)
+      const size_t np = (size_t)R * c * b;
+      auto xi = [&](size_t d, size_t r, size_t kk) { return (u32)(d * R * b + r * b + kk); };
       auto wi = [&](size_t d, size_t kk, size_t j) { return (u32)(nrow + d * nW + kk * c + j); };
       size_t terms_per_product;
       if (m == 5 || m == 7) {
@@ -202,12 +218,13 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
         std::vector<i64> coef(2 * np * 2);
         std::vector<u64> cst(2 * np, 0);
         std::vector<u32> ids(2 * np);
+        for (size_t r = 0; r < R; r++)
         for (size_t j = 0; j < c; j++)
           for (size_t kk = 0; kk < b; kk++) {
-            const size_t e = j * b + kk;
+            const size_t e = (r * c + j) * b + kk;
             for (int h = 0; h < 2; h++) {
               const size_t o = 2 * e + h;
-              idx[2 * o] = xi(0, kk);
+              idx[2 * o] = xi(0, r, kk);
               idx[2 * o + 1] = wi(0, kk, j);
               coef[2 * o] = 1;
               coef[2 * o + 1] = h ? -1 : 1;
@@ -228,13 +245,14 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
         std::vector<i64> coef(3 * np * 2);
         std::vector<u64> cst(3 * np, 0);
         std::vector<u32> ids(3 * np);
+        for (size_t r = 0; r < R; r++)
         for (size_t j = 0; j < c; j++)
           for (size_t kk = 0; kk < b; kk++) {
-            const size_t e = j * b + kk;
+            const size_t e = (r * c + j) * b + kk;
             const size_t da[3] = {0, 0, 1}, db[3] = {0, 1, 0};
             for (int h = 0; h < 3; h++) {
               const size_t o = 3 * e + h;
-              idx[2 * o] = xi(da[h], kk);
+              idx[2 * o] = xi(da[h], r, kk);
               idx[2 * o + 1] = wi(db[h], kk, j);
               coef[2 * o] = 4;
               coef[2 * o + 1] = 1;
@@ -255,12 +273,13 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
         std::vector<u32> idx(2 * np * 2);
         std::vector<i64> coef(2 * np * 2);
         std::vector<u64> cst(2 * np);
+        for (size_t r = 0; r < R; r++)
         for (size_t j = 0; j < c; j++)
           for (size_t kk = 0; kk < b; kk++) {
-            const size_t e = j * b + kk;
+            const size_t e = (r * c + j) * b + kk;
             for (int h = 0; h < 2; h++) {
               const size_t o = 2 * e + h;
-              idx[2 * o] = xi(0, kk);
+              idx[2 * o] = xi(0, r, kk);
               idx[2 * o + 1] = wi(0, kk, j);
               coef[2 * o] = 1;
               coef[2 * o + 1] = h ? -1 : 1;
@@ -294,18 +313,19 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
       }
       // ---------------- g3: modular summation of the b * terms_per_product terms of each output j
       const size_t terms = b * terms_per_product;
+      const size_t outs = (size_t)R * c;
       u64 *dst = out + ((size_t)mi * a + i) * c * ctw;
       if (m == 16) {
         // native wrap at scale 2^60: one linear op sums all terms
-        std::vector<u32> idx(c * terms);
-        std::vector<i64> coef(c * terms, 1);
-        std::vector<u64> cst(c, 0);
-        for (size_t j = 0; j < c; j++)
+        std::vector<u32> idx(outs * terms);
+        std::vector<i64> coef(outs * terms, 1);
+        std::vector<u64> cst(outs, 0);
+        for (size_t j = 0; j < outs; j++)
           for (size_t t = 0; t < terms; t++) idx[j * terms + t] = (u32)(j * terms + t);
-        if ((rc = linear(D, T1, dst, c, (int)terms, idx, coef, cst))) return rc;
+        if ((rc = linear(D, T1, dst, outs, (int)terms, idx, coef, cst))) return rc;
       } else {
-        if ((rc = sum_tree(D, m, T1, T0, T2, c, terms))) return rc;
-        SZ_CUDA_OK(cudaMemcpyAsync(dst, T1, c * ctw * 8, cudaMemcpyDeviceToDevice, D.st));
+        if ((rc = sum_tree(D, m, T1, T0, T2, outs, terms))) return rc;
+        SZ_CUDA_OK(cudaMemcpyAsync(dst, T1, outs * ctw * 8, cudaMemcpyDeviceToDevice, D.st));
       }
     }
   }

@@ -170,37 +170,63 @@ class Context:
         return self.pbs(s, [table16(lambda v: v, -8)])
 
     # ------------------------------------------------------- one training step
+    def _tick(self, times, name):
+        if times is not None:
+            import time
+            torch.cuda.synchronize()
+            now = time.perf_counter()
+            times[name] = times.get(name, 0.0) + now - times["_t"]
+            times["_t"] = now
+
     def train_step(self, A0, Y, Ws, cap: int = 7, keep=False):
         """A0 [a][b_1], Y [a][c_L] one-hot bits, Ws[l] [c_l][b_l] (ciphertexts
-        [..][dim+1] on the device) -> new weights (and intermediates if keep)."""
+        [..][dim+1] on the device) -> new weights (and intermediates if keep,
+        including a per-stage wall-time breakdown)."""
+        import time
         L = len(Ws)
         a = A0.shape[0]
         acts, pre, inter = [A0], [], {"pre": [], "acts": [], "errs": [], "grads": []}
+        times = {"_t": time.perf_counter()} if keep else None
+        tick = lambda name: self._tick(times, name)  # noqa: E731
         for l in range(L):
             W = Ws[l]
             c_l, b_l = W.shape[0], W.shape[1]
             base = get_rns_base(b_l * 64)
             res = self.matmul(acts[-1], W.transpose(0, 1), base)          # [k][a][c_l]
+            tick("forward matmul")
             S = self.shift2msbs(res.reshape(len(base), a * c_l, -1), base).reshape(a, c_l, -1)
+            tick("shift2msbs")
             pre.append(S)
             acts.append(self.relu_cap(S, cap).reshape(a, c_l, -1) if l < L - 1 else S)
+            tick("relu")
         E = sz.int_ce_grad(acts[-1].contiguous(), Y.contiguous(), self.ka["fbsk"], self.ka["ksk"], self.PA)
+        tick("ce grad")
         inter["errs"].append(E)
         newW = [None] * L
         for l in range(L - 1, -1, -1):
             W = Ws[l]
             c_l, b_l = W.shape[0], W.shape[1]
             gbase = get_rns_base(a * 8)
-            G = self.sign3(self.matmul(E.transpose(0, 1), acts[l], gbase).reshape(len(gbase), c_l * b_l, -1),
-                           gbase).reshape(c_l, b_l, -1)
+            Gm = self.matmul(E.transpose(0, 1), acts[l], gbase)
+            tick("backward matmul")
+            G = self.sign3(Gm.reshape(len(gbase), c_l * b_l, -1), gbase).reshape(c_l, b_l, -1)
+            tick("sign3")
             if l > 0:
                 ebase = get_rns_base(c_l * 8)
-                En = self.sign3(self.matmul(E, W, ebase).reshape(len(ebase), a * b_l, -1), ebase)
+                Em = self.matmul(E, W, ebase)
+                tick("backward matmul")
+                En = self.sign3(Em.reshape(len(ebase), a * b_l, -1), ebase)
+                tick("sign3")
                 E = self.relu_mask(En, pre[l - 1].reshape(a * b_l, -1), cap).reshape(a, b_l, -1)
+                tick("relu")
                 inter["errs"].append(E)
             inter["grads"].insert(0, G)
             newW[l] = self.update(W.reshape(c_l * b_l, -1), G.reshape(c_l * b_l, -1)).reshape(c_l, b_l, -1)
+            tick("update")
         inter["pre"], inter["acts"] = pre, acts
+        if times is not None:
+            times.pop("_t")
+            inter["times"] = times
         return (newW, inter) if keep else newW
 
 

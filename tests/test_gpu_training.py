@@ -75,6 +75,7 @@ def test_train_step_paper_shaped_mlp(dev):
     parameter sets (n = 742 / 1024)."""
     ctx, newW, it, refW, ref, rep = run_step([28, 8, 2], 8, 92, dev, small_n=False)
     check(ctx, newW, it, refW, ref)
+    rep["stage_s"] = it["times"]
     rep.update({"workload": "Alg. 6 training step, MLP 28-8-2, batch 8, set A + set-B Shift2MSBs stage",
                 "weights_changed": [int((r != W0).sum()) for r, W0 in zip(refW, ref["W_in"])],
                 "pbs_set_a_outside_drivers": ctx.pbs_count})
