@@ -70,6 +70,26 @@ def test_train_step_tiny_small_n(dev):
     check(*run_step([6, 3, 2], 4, 91, dev, small_n=True)[:5])
 
 
+def test_train_steps_chain(dev):
+    """Two consecutive steps (R26): the second step starts from the encrypted
+    weights the first produced (fresh PBS outputs) and a new batch, and still
+    decrypts to the cleartext Alg. 6 everywhere."""
+    from paper_2504_17785_b200 import workload as wl
+    ctx, newW, it, refW, ref, _ = run_step([6, 3, 2], 4, 93, dev, small_n=True)
+    check(ctx, newW, it, refW, ref)
+    PA = ctx.PA
+    rng = streams(94)["messages"]
+    A0 = rng.integers(-8, 8, size=(4, 6))
+    Y = np.zeros((4, 2), dtype=np.int64)
+    Y[np.arange(4), rng.integers(0, 2, size=4)] = 1
+    key = ctx.ka["big_key"]
+    enc = lambda x, s: wl.encrypt(PA, np.asarray(x).reshape(-1), lwe_randomness(PA, np.asarray(x).size, s), key,  # noqa: E731
+                                  dev).reshape(*np.asarray(x).shape, -1)
+    newW2, it2 = ctx.train_step(enc(A0, 95), enc(Y, 96), newW, keep=True)
+    refW2, ref2 = G.train_step(A0, Y, refW)
+    check(ctx, newW2, it2, refW2, ref2)
+
+
 def test_train_step_paper_shaped_mlp(dev):
     """The paper's smallest MLP shape (28-8-2, batch 8) at the full
     parameter sets (n = 742 / 1024)."""
