@@ -165,13 +165,13 @@ int silenzio_mrns_bitlen_max(const uint64_t *digits, uint32_t k, size_t count, u
   if (count == 0) return SILENZIO_OK;
   const size_t cw = ct_bytes(P) / 8;
   unsigned char *p = reinterpret_cast<unsigned char *>(workspace);
+  u64 *buf = reinterpret_cast<u64 *>(p);   // [k][count] working copy of the bit lengths
   p += rup((size_t)k * count * cw * 8);
-  u64 *buf = reinterpret_cast<u64 *>(p);
-  p += rup(count * cw * 8);
-  u64 *tmp = reinterpret_cast<u64 *>(p);
-  p += rup(count * cw * 8);
-  u64 *tmp2 = reinterpret_cast<u64 *>(p);
-  p += 4 * rup(count * cw * 8);
+  u64 *tmp = reinterpret_cast<u64 *>(p);   // [k][count / 2] (k <= 6 fits the 3 count reserved)
+  p += 3 * rup(count * cw * 8);
+  u64 *tmp2 = reinterpret_cast<u64 *>(p);  // [k][count / 2]
+  p += 3 * rup(count * cw * 8);
+  if (k > 6) return SILENZIO_ERR_UNSUPPORTED;
   Dev D;
   dev_init(D, p, P, fbsk, ksk, sz_stream(stream), 4 * count + 64);
   int rc;
@@ -179,22 +179,30 @@ int silenzio_mrns_bitlen_max(const uint64_t *digits, uint32_t k, size_t count, u
   if ((rc = upload_luts(D, tb))) return rc;
   if ((rc = lookup(D, digits, bitlen_out, (size_t)k * count, {}, 1))) return rc;
   std::vector<std::vector<u64>> trelu = {table_window(-8, [](int d) { return enc(d > 0 ? d : 0, kDelta); })};
-  for (uint32_t i = 0; i < k; i++) {
-    // max tree (T7): max(a, b) = b + ReLU(a - b), first half against second half
-    SZ_CUDA_OK(cudaMemcpyAsync(buf, bitlen_out + (size_t)i * count * cw, count * cw * 8, cudaMemcpyDeviceToDevice, D.st));
-    size_t cur = count;
-    while (cur > 1) {
-      const size_t half = cur / 2;
-      if ((rc = axpy3(D, tmp, buf, 1, buf + half * cw, -1, nullptr, 0, 0, half))) return rc;
-      if ((rc = upload_luts(D, trelu))) return rc;
-      if ((rc = lookup(D, tmp, tmp2, half, {}, 1))) return rc;
-      if ((rc = axpy3(D, buf, buf + half * cw, 1, tmp2, 1, nullptr, 0, 0, half))) return rc;
-      if (cur & 1)
-        SZ_CUDA_OK(cudaMemcpyAsync(buf + half * cw, buf + (cur - 1) * cw, cw * 8, cudaMemcpyDeviceToDevice, D.st));
-      cur = half + (cur & 1);
+  if ((rc = upload_luts(D, trelu))) return rc;
+  // max tree (T7) per digit position: max(a, b) = b + ReLU(a - b), first half
+  // against second half; the k positions advance level by level together (one
+  // PBS batch per level, positions at stride `count` in buf)
+  SZ_CUDA_OK(cudaMemcpyAsync(buf, bitlen_out, (size_t)k * count * cw * 8, cudaMemcpyDeviceToDevice, D.st));
+  size_t cur = count;
+  while (cur > 1) {
+    const size_t half = cur / 2;
+    for (uint32_t i = 0; i < k; i++) {
+      u64 *bi = buf + (size_t)i * count * cw;
+      if ((rc = axpy3(D, tmp + (size_t)i * half * cw, bi, 1, bi + half * cw, -1, nullptr, 0, 0, half))) return rc;
     }
-    SZ_CUDA_OK(cudaMemcpyAsync(max_out + (size_t)i * cw, buf, cw * 8, cudaMemcpyDeviceToDevice, D.st));
+    if ((rc = lookup(D, tmp, tmp2, (size_t)k * half, {}, 1))) return rc;
+    for (uint32_t i = 0; i < k; i++) {
+      u64 *bi = buf + (size_t)i * count * cw;
+      if ((rc = axpy3(D, bi, bi + half * cw, 1, tmp2 + (size_t)i * half * cw, 1, nullptr, 0, 0, half))) return rc;
+      if (cur & 1)
+        SZ_CUDA_OK(cudaMemcpyAsync(bi + half * cw, bi + (cur - 1) * cw, cw * 8, cudaMemcpyDeviceToDevice, D.st));
+    }
+    cur = half + (cur & 1);
   }
+  for (uint32_t i = 0; i < k; i++)
+    SZ_CUDA_OK(cudaMemcpyAsync(max_out + (size_t)i * cw, buf + (size_t)i * count * cw, cw * 8, cudaMemcpyDeviceToDevice,
+                               D.st));
   return SILENZIO_OK;
 }
 
