@@ -29,38 +29,66 @@ int bitlen(int d) {
 
 long rhe(double x) { return (long)nearbyint(x); }  // round half to even (default FE_TONEAREST)
 
-// Alg. 1 on device buffers; `out` may not alias `in`. tmp*: count ciphertexts each.
+// Alg. 1 on device buffers; `out` may not alias `in`. tmp holds tcap,
+// tmp2 / tmp3 hold tcap2 ciphertexts (each >= count). For pivot i the targets
+// j >= i are independent: consecutive targets are evaluated together (one PBS
+// batch per group, one LUT per target via lut ids), as many as the scratch and
+// the kMaxLuts test polynomials allow. Every ciphertext sees exactly the
+// operations of the one-target-at-a-time schedule.
 int rns2mrns_impl(Dev &D, const u64 *in, const uint32_t *moduli, int k, size_t count, u64 *out, u64 *tmp,
-                  u64 *tmp2, u64 *tmp3) {
+                  u64 *tmp2, u64 *tmp3, size_t tcap, size_t tcap2) {
   const size_t cw = D.big;
   SZ_CUDA_OK(cudaMemcpyAsync(out, in, (size_t)k * count * cw * 8, cudaMemcpyDeviceToDevice, D.st));
   int rc;
   for (int i = 1; i < k; i++) {
     const int mp = (int)moduli[i - 1];
     const u64 *pivot = out + (size_t)(i - 1) * count * cw;
-    for (int j = i; j < k; j++) {
-      const int mj = (int)moduli[j];
-      const int t = inv_mod(mp, mj);
-      u64 *yj = out + (size_t)j * count * cw;
+    int j0 = i;
+    while (j0 < k) {
+      // group [j0, j1): same kind (direct window or T3), within scratch and LUT capacity
+      const bool direct = mp + (int)moduli[j0] - 1 <= 16;
+      const size_t cap = direct ? tcap : tcap2;
+      int j1 = j0 + 1;
+      while (j1 < k && j1 - j0 < kMaxLuts && (size_t)(j1 - j0 + 1) * count <= cap &&
+             (mp + (int)moduli[j1] - 1 <= 16) == direct)
+        j1++;
+      const int ng = j1 - j0;
+      std::vector<u32> ids((size_t)ng * count);
+      for (int g = 0; g < ng; g++) std::fill(ids.begin() + (size_t)g * count, ids.begin() + (size_t)(g + 1) * count, (u32)g);
       // d = y_j - y_{i-1} in [-(mp-1), mj-1]
-      if ((rc = axpy3(D, tmp, yj, 1, pivot, -1, nullptr, 0, 0, count))) return rc;
-      if (mp + mj - 1 <= 16) {
-        std::vector<std::vector<u64>> tabs = {
-            table_window(-(mp - 1), [mj, t](int d) { return enc(pmod((long)d * t, mj), kDelta); })};
+      for (int g = 0; g < ng; g++) {
+        u64 *yj = out + (size_t)(j0 + g) * count * cw;
+        if ((rc = axpy3(D, tmp + (size_t)g * count * cw, yj, 1, pivot, -1, nullptr, 0, 0, count))) return rc;
+      }
+      u64 *yout = out + (size_t)j0 * count * cw;  // targets j0.. are consecutive in out
+      if (direct) {
+        std::vector<std::vector<u64>> tabs;
+        for (int g = 0; g < ng; g++) {
+          const int mj = (int)moduli[j0 + g], t = inv_mod(mp, mj);
+          tabs.push_back(table_window(-(mp - 1), [mj, t](int d) { return enc(pmod((long)d * t, mj), kDelta); }));
+        }
         if ((rc = upload_luts(D, tabs))) return rc;
-        if ((rc = lookup(D, tmp, yj, count, {}, 1))) return rc;
+        if ((rc = lookup(D, tmp, yout, (size_t)ng * count, ids, (u32)ng))) return rc;
       } else {
         // T3: u = d mod mj = d + mj Delta/2 - sign(d) mj Delta/2 ; then T1 on [0,16)
-        const u64 half = (u64)mj * (kDelta >> 1);
-        std::vector<std::vector<u64>> tabs = {std::vector<u64>(16, half)};
+        std::vector<std::vector<u64>> tabs;
+        for (int g = 0; g < ng; g++) tabs.push_back(std::vector<u64>(16, (u64)moduli[j0 + g] * (kDelta >> 1)));
         if ((rc = upload_luts(D, tabs))) return rc;
-        if ((rc = lookup(D, tmp, tmp2, count, {}, 1))) return rc;
-        if ((rc = axpy3(D, tmp3, tmp, 1, tmp2, -1, nullptr, 0, half, count))) return rc;
-        std::vector<std::vector<u64>> tabs2 = {
-            table_window(0, [mj, t](int u) { return enc(pmod((long)u * t, mj), kDelta); })};
+        if ((rc = lookup(D, tmp, tmp2, (size_t)ng * count, ids, (u32)ng))) return rc;
+        for (int g = 0; g < ng; g++) {
+          const u64 half = (u64)moduli[j0 + g] * (kDelta >> 1);
+          const size_t o = (size_t)g * count * cw;
+          if ((rc = axpy3(D, tmp3 + o, tmp + o, 1, tmp2 + o, -1, nullptr, 0, half, count))) return rc;
+        }
+        std::vector<std::vector<u64>> tabs2;
+        for (int g = 0; g < ng; g++) {
+          const int mj = (int)moduli[j0 + g], t = inv_mod(mp, mj);
+          tabs2.push_back(table_window(0, [mj, t](int u) { return enc(pmod((long)u * t, mj), kDelta); }));
+        }
         if ((rc = upload_luts(D, tabs2))) return rc;
-        if ((rc = lookup(D, tmp3, yj, count, {}, 1))) return rc;
+        if ((rc = lookup(D, tmp3, yout, (size_t)ng * count, ids, (u32)ng))) return rc;
       }
+      j0 = j1;
     }
   }
   return SILENZIO_OK;
@@ -99,16 +127,15 @@ int silenzio_rns2mrns(const uint64_t *in, const uint32_t *moduli_host, uint32_t 
   if (count == 0) return SILENZIO_OK;
   unsigned char *p = reinterpret_cast<unsigned char *>(workspace);
   const size_t ct = ct_bytes(P);
-  p += rup((size_t)k * count * ct);  // (digits slot unused here)
-  u64 *t0 = reinterpret_cast<u64 *>(p);
-  p += rup(count * ct);
-  u64 *t1 = reinterpret_cast<u64 *>(p);
-  p += rup(count * ct);
-  u64 *t2 = reinterpret_cast<u64 *>(p);
-  p += 4 * rup(count * ct);
+  u64 *t0 = reinterpret_cast<u64 *>(p);  // k count (the digits slot is free here)
+  p += rup((size_t)k * count * ct);
+  u64 *t1 = reinterpret_cast<u64 *>(p);  // 3 count
+  p += 3 * rup(count * ct);
+  u64 *t2 = reinterpret_cast<u64 *>(p);  // 3 count
+  p += 3 * rup(count * ct);
   Dev D;
   dev_init(D, p, P, fbsk, ksk, sz_stream(stream), 4 * count + 64);
-  return rns2mrns_impl(D, in, moduli_host, (int)k, count, out, t0, t1, t2);
+  return rns2mrns_impl(D, in, moduli_host, (int)k, count, out, t0, t1, t2, (size_t)k * count, 3 * count);
 }
 
 int silenzio_rns_sign_abs(const uint64_t *in, const uint32_t *moduli_host, uint32_t k, size_t count,
@@ -132,7 +159,7 @@ int silenzio_rns_sign_abs(const uint64_t *in, const uint32_t *moduli_host, uint3
   }
   Dev D;
   dev_init(D, p, P, fbsk, ksk, sz_stream(stream), 4 * count + 64);
-  if ((rc = rns2mrns_impl(D, in, moduli_host, (int)k, count, digits, t[0], t[1], t[2]))) return rc;
+  if ((rc = rns2mrns_impl(D, in, moduli_host, (int)k, count, digits, t[0], t[2], t[4], 2 * count, 2 * count))) return rc;
   // e = [top digit >= r_k / 2]  (0 or 1 at Delta)
   const int rk = (int)moduli_host[k - 1];
   std::vector<std::vector<u64>> st = {table_window(0, [rk](int y) { return enc(2 * y >= rk ? 1 : 0, kDelta); })};
