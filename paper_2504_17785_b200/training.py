@@ -122,15 +122,21 @@ class Context:
         hi = self.pbs(x, [table16(lambda v: v // 2 + 4, 0)])
         return self.lin([(1, hi), (1, sp)])
 
-    def shift2msbs(self, res, base):
+    def shift2msbs(self, res, base, times=None):
         """Shift2MSBs+- (Alg. 4) to Gamma = 4: residues [k][count] -> [count] in [-7, 7]."""
         ka = self.ka
+        tick = lambda name: self._tick(times, name)  # noqa: E731
         digits = sz.rns2mrns(res, base, ka["fbsk"], ka["ksk"], self.PA)
+        tick("s2m rns2mrns")
         _, absr = sz.rns_sign_abs(res, base, ka["fbsk"], ka["ksk"], self.PA)
+        tick("s2m sign_abs")
         dabs = sz.rns2mrns(absr, base, ka["fbsk"], ka["ksk"], self.PA)
+        tick("s2m rns2mrns")
         _, mx = sz.mrns_bitlen_max(dabs, ka["fbsk"], ka["ksk"], self.PA)
+        tick("s2m bitlen_max")
         Y, _ = sz.mrns_digit_combine(digits[-1].contiguous(), dabs, mx, base[-1], W_BITS, 3, ka, self.PA,
                                      self.kb, self.PB, self.ksk_ab, self.pab, self.ksk_ba, self.pba)
+        tick("s2m digit_combine (set B)")
         return Y
 
     def sign3(self, res, base):
@@ -194,8 +200,7 @@ class Context:
             base = get_rns_base(b_l * 64)
             res = self.matmul(acts[-1], W.transpose(0, 1), base)          # [k][a][c_l]
             tick("forward matmul")
-            S = self.shift2msbs(res.reshape(len(base), a * c_l, -1), base).reshape(a, c_l, -1)
-            tick("shift2msbs")
+            S = self.shift2msbs(res.reshape(len(base), a * c_l, -1), base, times).reshape(a, c_l, -1)
             pre.append(S)
             acts.append(self.relu_cap(S, cap).reshape(a, c_l, -1) if l < L - 1 else S)
             tick("relu")
