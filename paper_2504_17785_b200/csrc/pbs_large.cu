@@ -169,9 +169,6 @@ __device__ __forceinline__ u64 limb_to_torus_L(double x, int p, int P, int w) {
 #define SZ_SETC_TMEM 1  // digit spectra in TMEM instead of (L2-backed) local memory
 #endif
 
-#ifndef SZ_SETC_MAC2
-#define SZ_SETC_MAC2 0  // measured 1.66k vs 2.80k PBS/s (spills in the hot loop); MAC: all rows' BSK loads of a slot group in flight together
-#endif
 
 struct BRLArgs {
   const u64 *lwe_small;
@@ -184,27 +181,10 @@ struct BRLArgs {
   int n, base_log, w;
 };
 
-#ifndef SZ_SETC_ASYNC
-#define SZ_SETC_ASYNC 0  // measured 2.33k vs 2.80k PBS/s (LDGSTS + LDS double the shared-memory wavefronts); MAC: per-thread cp.async ring streaming the Fourier BSK 8 values ahead
-#endif
-constexpr int kRing = 8;  // BSK values in flight per thread (ring slots)
-
-// ring only on the TMEM-spectra path (rows <= 4)
-__host__ __device__ constexpr size_t brl_smem_bytes(int n, int rows = 4) {
-  return 2 * kNL * sizeof(u64) + kML * sizeof(double2) + ((size_t)n * 2 + 15) / 16 * 16 +
-         ((SZ_SETC_ASYNC && rows <= 4) ? (size_t)kRing * kTL * sizeof(double2) : 0);
+__host__ __device__ constexpr size_t brl_smem_bytes(int n) {
+  return 2 * kNL * sizeof(u64) + kML * sizeof(double2) + ((size_t)n * 2 + 15) / 16 * 16;
 }
 
-// per-thread asynchronous global -> shared copies (LDGSTS, L1 bypass); each
-// thread waits only for its own copies, so the ring needs no CTA barrier
-__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-  asm volatile("cp.async.commit_group;" ::: "memory");
-}
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 template <int L, int P>
 __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
@@ -215,12 +195,6 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
   unsigned short *abar = reinterpret_cast<unsigned short *>(buf + kML);
   const int t = threadIdx.x;
   const int n = A.n, w = A.w, blog = A.base_log;
-  // BSK ring [kRing][256] after abar: value sl of a (i, o, p, row) block lives in slot sl % kRing
-  double2 *ring = reinterpret_cast<double2 *>(reinterpret_cast<unsigned char *>(abar) + ((size_t)n * 2 + 15) / 16 * 16);
-  // the stream of (i, o, p, row) blocks in MAC order: o, p = P-1..0, row
-  auto row_ptr = [&](int i, int o, int p, int row) {
-    return A.fbsk + ((((size_t)i * 2 + o) * rows + row) * P + p) * kML + t;
-  };
   // thread-private digit spectra: in tensor memory when they fit (rows <= 4:
   // threads t and t + 128 share a lane (warps w, w + 4), columns [0, 256) and
   // [256, 512); row r, slot sl at column 64 r + 4 sl), else in local memory
@@ -235,12 +209,6 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
   }
   const uint32_t ta_spec = kTm ? tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16) + 256 * (wid >> 2) : 0u;
   double2 spec[kTm ? 1 : rows][16];
-  constexpr bool kAsync = SZ_SETC_ASYNC && kTm;
-  const double2 *Gcur = row_ptr(0, 0, P - 1, 0);  // block being consumed by the ring
-  if constexpr (kAsync) {
-#pragma unroll
-    for (int sl = 0; sl < kRing; sl++) cp_async16(ring + sl * kTL + t, Gcur + sl * kTL);
-  }
   for (long c = blockIdx.x; c < A.count; c += gridDim.x) {
     const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
     for (int i = t; i < n; i += kTL) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2NL);
@@ -310,69 +278,6 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
           double2 y[16];
 #pragma unroll
           for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
-          if constexpr (kAsync) {
-            // values arrive in consumption order through the ring; the copy for
-            // value sl + 8 (or value sl - 8 of the next block in the stream,
-            // wrapping from BSK_{n-1} to BSK_0) is issued as value sl is used
-#pragma unroll 1
-            for (int row = 0; row < rows; row++) {
-              int ni = i, no = o, np = p, nr = row + 1;
-              if (nr == rows) {
-                nr = 0;
-                if (np > 0) {
-                  np--;
-                } else {
-                  np = P - 1;
-                  if (no == 0) {
-                    no = 1;
-                  } else {
-                    no = 0;
-                    ni = (i + 1 == n) ? 0 : i + 1;
-                  }
-                }
-              }
-              const double2 *Gnext = row_ptr(ni, no, np, nr);
-#pragma unroll
-              for (int qq = 0; qq < 4; qq += 2) {
-                uint32_t d0[16], d1[16];
-                tmem_ld16(ta_spec + 64 * row + 16 * qq, d0);
-                tmem_ld16(ta_spec + 64 * row + 16 * (qq + 1), d1);
-                tmem_wait_ld16x2(d0, d1);
-#pragma unroll
-                for (int q = 0; q < 8; q++) {
-                  const int sl = 4 * qq + q;
-                  cp_async_wait<kRing - 1>();
-                  double2 *slot = ring + (sl % kRing) * kTL + t;
-                  const double2 g = *slot;
-                  cmac(y[sl], unpack1(q < 4 ? d0 : d1, q & 3), g);
-                  cp_async16(slot, sl < kRing ? Gcur + (sl + kRing) * kTL : Gnext + (sl - kRing) * kTL);
-                }
-              }
-              Gcur = Gnext;
-            }
-          } else
-#if SZ_SETC_MAC2
-          if constexpr (kTm) {
-            // all rows of a 4-slot group loaded together: rows x 4 BSK loads in
-            // flight per thread (the MAC is bound by their L2 latency)
-#pragma unroll
-            for (int qq = 0; qq < 4; qq++) {
-              double2 g[rows][4];
-#pragma unroll
-              for (int row = 0; row < rows; row++)
-#pragma unroll
-                for (int q = 0; q < 4; q++) g[row][q] = __ldg(&Gi[((size_t)row * P + p) * kML + (4 * qq + q) * kTL]);
-#pragma unroll
-              for (int row = 0; row < rows; row++) {
-                uint32_t d[16];
-                tmem_ld16(ta_spec + 64 * row + 16 * qq, d);
-                tmem_wait_ld16(d);
-#pragma unroll
-                for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], unpack1(d, q), g[row][q]);
-              }
-            }
-          } else
-#endif
 #pragma unroll 1
           for (int row = 0; row < rows; row++) {
             const double2 *G = Gi + ((size_t)row * P + p) * kML;
@@ -487,7 +392,7 @@ int launch_blind_rotate_large(const u64 *lwe_small, const u32 *lut_ids, const u6
   SZ_BRL_CASE(1, 3) SZ_BRL_CASE(2, 3) SZ_BRL_CASE(2, 2) SZ_BRL_CASE(2, 1) SZ_BRL_CASE(3, 3) SZ_BRL_CASE(4, 3)
 #undef SZ_BRL_CASE
   if (!kern) return SILENZIO_ERR_UNSUPPORTED;
-  const size_t smem = brl_smem_bytes(A.n, 2 * L);
+  const size_t smem = brl_smem_bytes(A.n);
   if (smem > 227 * 1024) return SILENZIO_ERR_UNSUPPORTED;
   SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long wave = blind_rotate_large_wave(P);
