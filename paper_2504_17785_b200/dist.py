@@ -41,3 +41,31 @@ def sum_over_ranks(x: int, device=None) -> int:
 def aggregate_throughput(world: int, batch_per_rank: int, steps: int, max_seconds: float) -> float:
     """Whole-job PBS/s: units all ranks processed / the slowest rank's time."""
     return world * batch_per_rank * steps / max_seconds
+
+
+# ---------------------------------------------------- gadget-layer sharding
+# SURVEY.md §8(e): Matmul^RNS (config 3) shards by modulus -- the k residue
+# channels are independent -- with the keys replicated on every rank; the only
+# collective is one all-gather of the residue ciphertexts at the end.
+def shard_moduli(moduli, world: int, rank: int):
+    """Round-robin modulus channels of this rank: (indices, moduli)."""
+    idx = list(range(rank, len(moduli), world))
+    return idx, [moduli[i] for i in idx]
+
+
+def gather_channels(local: torch.Tensor, k: int, world: int, rank: int) -> torch.Tensor:
+    """local [k_rank][...] residue ciphertexts of this rank's channels ->
+    [k][...] on every rank, channels back in modulus order (all_gather of
+    equal-sized, zero-padded slabs)."""
+    per = (k + world - 1) // world
+    slab = torch.zeros((per,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    slab[: local.shape[0]] = local
+    if world == 1:
+        return slab[:k].clone()
+    parts = [torch.empty_like(slab) for _ in range(world)]
+    dist.all_gather(parts, slab)
+    out = torch.empty((k,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    for r in range(world):
+        idx = list(range(r, k, world))
+        out[idx] = parts[r][: len(idx)]
+    return out

@@ -72,3 +72,37 @@ def test_shard_bounds_cover_exactly():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             sizes = [hi - lo for lo, hi in spans]
             assert max(sizes) - min(sizes) <= 1
+
+
+def _worker_moduli(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        base = [5, 7, 9, 11, 13, 16]
+        idx, mods = sdist.shard_moduli(base, world, rank)
+        # stand-in for this rank's Matmul^RNS channels: residue "ciphertexts" tagged by modulus
+        local = torch.stack([torch.full((2, 3, 4), m, dtype=torch.int64) for m in mods])
+        full = sdist.gather_channels(local, len(base), world, rank)
+        q.put((rank, idx, [int(full[i, 0, 0, 0]) for i in range(len(base))]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_modulus_sharding():
+    """Config-3 sharding by modulus: the ranks' channels partition
+    the base and the all-gather returns every channel in modulus order."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_moduli, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert sorted(res[0][1] + res[1][1]) == list(range(6))
+    for _, _, order in res:
+        assert order == [5, 7, 9, 11, 13, 16]

@@ -16,7 +16,15 @@ from synth import get_params, key_randomness, lwe_randomness, streams  # noqa: E
 
 a, b, c = [int(v) for v in (sys.argv[1:4] if len(sys.argv) >= 4 else (16, 784, 64))]
 BASE = [5, 7, 9, 11, 13, 16]
-dev = torch.device("cuda:0")
+# multi-GPU (torchrun): the modulus channels are sharded over the ranks
+# (SURVEY.md §8(e)); keys and inputs are replicated from the same seeds
+from paper_2504_17785_b200 import dist as sdist  # noqa: E402
+WORLD, RANK = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+if WORLD > 1:
+    import torch.distributed as tdist
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    tdist.init_process_group("nccl")
+dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
 P = get_params("A")
 rnd = key_randomness(P, 3)
 keys = wl.device_keys(P, rnd, dev)
@@ -31,11 +39,16 @@ torch.cuda.synchronize()
 t0 = time.perf_counter()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-out = silenzio.rns_matmul(Xc, Wc, BASE, keys["fbsk"], keys["ksk"], P)
+_, my_mods = sdist.shard_moduli(BASE, WORLD, RANK)
+local = silenzio.rns_matmul(Xc, Wc, my_mods, keys["fbsk"], keys["ksk"], P)
 e1.record()
 torch.cuda.synchronize()
+ms = sdist.max_over_ranks(e0.elapsed_time(e1), device=dev)
+out = sdist.gather_channels(local, len(BASE), WORLD, RANK)
+torch.cuda.synchronize()
 wall = time.perf_counter() - t0
-ms = e0.elapsed_time(e1)
+if RANK != 0:
+    sys.exit(0)
 ph = wl.to_host_u64(silenzio.lwe_phase_batch(out.reshape(-1, P.big_dim + 1), keys["big_key"])).reshape(len(BASE), a, c)
 res = []
 for mi, m in enumerate(BASE):
@@ -55,5 +68,6 @@ ref = X @ W
 mism = int((val != ref).sum())
 pbs = (a * b + b * c) * 7 + a * b * c * (2 + 2 + 4 * 3 + 3)
 print(json.dumps({"workload": f"configs[3] Matmul^RNS {a}x{b} . {b}x{c}, base {BASE}, set A",
+                  "n_gpus": WORLD, "sharding": "modulus channels round-robin over ranks",
                   "gadget_layer_s": ms / 1e3, "wall_s": wall, "outputs": int(res.size),
                   "crt_mismatches": mism, "max_abs_xw": int(np.abs(ref).max())}))
