@@ -234,6 +234,40 @@ int silenzio_mrns_digit_combine(const uint64_t *top_digit, const uint64_t *abs_d
                                 const uint64_t *ksk_ab, const silenzio_params *pab, const uint64_t *ksk_ba,
                                 const silenzio_params *pba, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Training-step gadgets (Alg. 6, l.466-502; SURVEY.md §8(f) NEXT #1;
+ * schedules DESIGN.md §6b'', readings R23-R26) at parameter set A. Thin
+ * drivers over linear LWE ops and PBS; ciphertext arrays are big-key LWE
+ * [*][kN+1] at Delta = 2^59 unless stated; workspace >=
+ * silenzio_train_workspace_bytes(params, k, count) (k = 1 except sign3);
+ * calls synchronise `stream`; shapes without a 16-value window schedule
+ * return SILENZIO_ERR_WINDOW.
+ *  silenzio_channel16     in [count]: residue r in [0,16) at 2^60 (the m = 16
+ *                         channel of silenzio_rns_matmul) -> out: r at Delta (2 PBS).
+ *  silenzio_rns_sign3     Sign^RNS_(-1,0,1) (l.309-323, zero test l.313): residues
+ *                         [k][count] at Delta, moduli ascending with 16 last, k <= 7
+ *                         -> out [count] in {-1, 0, 1}.
+ *  silenzio_relu_cap      ReLU_x(x) = min(max(x, 0), cap) (l.269-274), x in [-8, 8),
+ *                         0 <= cap <= 7.
+ *  silenzio_relu_mask     out = e [0 < s < cap] for e in {-1, 0, 1}, s in [-8, 8)
+ *                         (the ReLU_x derivative applied to an error sign, R25).
+ *  silenzio_weight_update out = clip(w - g, wmin, wmax) for w in [wmin, wmax] within
+ *                         [-8, 8), g in {-1, 0, 1}; fresh output (identity refresh). */
+size_t silenzio_train_workspace_bytes(const silenzio_params *params, uint32_t k, size_t count);
+int silenzio_channel16(const uint64_t *in, size_t count, uint64_t *out, const void *fbsk, const uint64_t *ksk,
+                       const silenzio_params *params, void *workspace, size_t workspace_bytes, void *stream);
+int silenzio_rns_sign3(const uint64_t *residues, const uint32_t *moduli_host, uint32_t k, size_t count,
+                       uint64_t *out, const void *fbsk, const uint64_t *ksk, const silenzio_params *params,
+                       void *workspace, size_t workspace_bytes, void *stream);
+int silenzio_relu_cap(const uint64_t *in, size_t count, int32_t cap, uint64_t *out, const void *fbsk,
+                      const uint64_t *ksk, const silenzio_params *params, void *workspace, size_t workspace_bytes,
+                      void *stream);
+int silenzio_relu_mask(const uint64_t *e, const uint64_t *s, size_t count, int32_t cap, uint64_t *out,
+                       const void *fbsk, const uint64_t *ksk, const silenzio_params *params, void *workspace,
+                       size_t workspace_bytes, void *stream);
+int silenzio_weight_update(const uint64_t *w, const uint64_t *g, size_t count, int32_t wmin, int32_t wmax,
+                           uint64_t *out, const void *fbsk, const uint64_t *ksk, const silenzio_params *params,
+                           void *workspace, size_t workspace_bytes, void *stream);
+
 /* ------------------------------------- client-side key / ciphertext generation
  * All random numbers are inputs (drawn by the caller), so every key and
  * ciphertext is a deterministic function of the caller's seeded draws. */

@@ -67,6 +67,12 @@ def load():
         "silenzio_int_ce_grad": ([V, V, U32, U32, V, V, V, P, V, S, V], I),
         "silenzio_mrns_combine_workspace_bytes": ([P, P, U32, S], S),
         "silenzio_mrns_digit_combine": ([V, V, V, U32, S, U32, U32, U32, V, V, V, V, P, V, P, V, P, V, P, V, S, V], I),
+        "silenzio_train_workspace_bytes": ([P, U32, S], S),
+        "silenzio_channel16": ([V, S, V, V, V, P, V, S, V], I),
+        "silenzio_rns_sign3": ([V, V, U32, S, V, V, V, P, V, S, V], I),
+        "silenzio_relu_cap": ([V, S, ctypes.c_int32, V, V, V, P, V, S, V], I),
+        "silenzio_relu_mask": ([V, V, S, ctypes.c_int32, V, V, V, P, V, S, V], I),
+        "silenzio_weight_update": ([V, V, S, ctypes.c_int32, ctypes.c_int32, V, V, V, P, V, S, V], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -87,6 +93,8 @@ def exported_symbols():
         "silenzio_rns_matmul", "silenzio_gadget_workspace_bytes", "silenzio_rns2mrns",
         "silenzio_rns_sign_abs", "silenzio_mrns_bitlen_max", "silenzio_int_ce_grad",
         "silenzio_mrns_combine_workspace_bytes", "silenzio_mrns_digit_combine",
+        "silenzio_train_workspace_bytes", "silenzio_channel16", "silenzio_rns_sign3", "silenzio_relu_cap",
+        "silenzio_relu_mask", "silenzio_weight_update",
     ]
 
 
@@ -373,3 +381,62 @@ def mrns_digit_combine(top_digit, abs_digits, maxes, top_radix, w, gamma, keys_a
         _ptr(keys_a["fbsk"]), _ptr(keys_a["ksk"]), ctypes.byref(pa), _ptr(keys_b["fbsk"]), ctypes.byref(pb),
         _ptr(ksk_ab), ctypes.byref(pab), _ptr(ksk_ba), ctypes.byref(pba), _ptr(ws), ws.numel(), _stream(stream)))
     return out, mb
+
+
+# ------------------------------------------------------ training-step gadgets
+def _tws(P, k, count, device):
+    n = load().silenzio_train_workspace_bytes(ctypes.byref(make_params(P)), k, count)
+    return torch.empty(n, dtype=torch.uint8, device=device)
+
+
+def _rows(t, P):
+    return t.reshape(-1, P.k * P.N + 1).contiguous()
+
+
+def channel16(z, fourier_bsk, ksk, P, stream=None):
+    """r at 2^60 (m = 16 channel of rns_matmul) -> r at Delta; z [..][kN+1]."""
+    z = _rows(z, P)
+    out = torch.empty_like(z)
+    ws = _tws(P, 1, z.shape[0], z.device)
+    _check(load().silenzio_channel16(_ptr(z), z.shape[0], _ptr(out), _ptr(fourier_bsk), _ptr(ksk),
+                                     ctypes.byref(make_params(P)), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def rns_sign3(residues, moduli, fourier_bsk, ksk, P, stream=None):
+    """Sign^RNS_(-1,0,1): residues [k][count] (all at Delta) -> [count] in {-1, 0, 1}."""
+    k, count = int(residues.shape[0]), int(residues.shape[1])
+    res = residues.reshape(k, count, -1).contiguous()
+    out = torch.empty((count, res.shape[-1]), dtype=torch.int64, device=res.device)
+    ws = _tws(P, k, count, res.device)
+    _check(load().silenzio_rns_sign3(_ptr(res), _moduli(moduli), k, count, _ptr(out), _ptr(fourier_bsk), _ptr(ksk),
+                                     ctypes.byref(make_params(P)), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def relu_cap(x, cap, fourier_bsk, ksk, P, stream=None):
+    x = _rows(x, P)
+    out = torch.empty_like(x)
+    ws = _tws(P, 1, x.shape[0], x.device)
+    _check(load().silenzio_relu_cap(_ptr(x), x.shape[0], int(cap), _ptr(out), _ptr(fourier_bsk), _ptr(ksk),
+                                    ctypes.byref(make_params(P)), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def relu_mask(e, s, cap, fourier_bsk, ksk, P, stream=None):
+    e, s = _rows(e, P), _rows(s, P)
+    out = torch.empty_like(e)
+    ws = _tws(P, 1, e.shape[0], e.device)
+    _check(load().silenzio_relu_mask(_ptr(e), _ptr(s), e.shape[0], int(cap), _ptr(out), _ptr(fourier_bsk),
+                                     _ptr(ksk), ctypes.byref(make_params(P)), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
+def weight_update(w, g, wmin, wmax, fourier_bsk, ksk, P, stream=None):
+    w, g = _rows(w, P), _rows(g, P)
+    out = torch.empty_like(w)
+    ws = _tws(P, 1, w.shape[0], w.device)
+    _check(load().silenzio_weight_update(_ptr(w), _ptr(g), w.shape[0], int(wmin), int(wmax), _ptr(out),
+                                         _ptr(fourier_bsk), _ptr(ksk), ctypes.byref(make_params(P)), _ptr(ws),
+                                         ws.numel(), _stream(stream)))
+    return out

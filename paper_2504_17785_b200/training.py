@@ -1,15 +1,17 @@
 """One Silenzio training step (Alg. 6) on encrypted data.
 
-SURVEY.md §8(f) NEXT #1. A host-side schedule over the C ABI: every arithmetic
-step is a libsilenzio kernel launch (PBS, linear LWE combinations, Matmul^RNS,
-RNS2MRNS, the 8-bit digit combine, IntCELossDeriv); this module only builds
-LUT tables, sequences the calls and reshapes ciphertext arrays. There is no
-CPU fallback: without the CUDA library every call raises.
+SURVEY.md §8(f) NEXT #1. A host-side sequence of C-ABI gadget calls (every
+arithmetic step is a libsilenzio kernel launch: Matmul^RNS, RNS2MRNS,
+sign / abs, bit lengths + block max, the 8-bit digit combine, IntCELossDeriv,
+and the training gadgets of csrc/gadgets_train.cu); this module only orders
+the calls and reshapes ciphertext arrays. There is no CPU fallback: without
+the CUDA library every call raises.
 
 Widths and readings (R23-R26): parameter set A (4-bit messages +
 padding, Delta = 2^59) for every LUT except the 8-bit MRNS digit combine of
 Shift2MSBs+- (set B); alpha = beta = Gamma = 4, ReLU cap x = 7, weights clipped
-to [-8, 7]; getRNSBase over {5, 7, 9, 11, 13} + 16. New 4-bit gadgets here:
+to [-8, 7]; getRNSBase over {5, 7, 9, 11, 13} + 16. New 4-bit gadgets
+(C ABI, csrc/gadgets_train.cu):
   * channel16: the m = 16 residue Matmul^RNS emits at 2^60 -> Delta (2 PBS),
   * sign3: Sign^RNS_(-1,0,1): top MRNS digit >= 8 and the zero
     test (sum of [digit != 0] over the digits) packed into one PBS,
@@ -26,7 +28,6 @@ import torch
 from . import silenzio as sz
 from . import workload as wl
 
-DLOG = 59            # set A: Delta = 2^59
 W_BITS = 4           # RNS modulus bit width w of Shift2MSBs
 BASES4 = [(13, 16), (11, 13, 16), (9, 11, 13, 16), (7, 9, 11, 13, 16), (5, 7, 9, 11, 13, 16)]
 
@@ -39,25 +40,6 @@ def get_rns_base(max_abs: int):
     raise ValueError("no 4-bit RNS base covers the range")
 
 
-def _u64(v: int) -> int:
-    return int(v) % (1 << 64)
-
-
-def table16(fn, w0: int, scale_log: int = DLOG) -> np.ndarray:
-    """16 torus values realising fn on the input window [w0, w0 + 16) of Z_32:
-    index x mod 32 < 16 reads T[x mod 32], otherwise -T[x mod 32 - 16]
-    (negacyclic test polynomial). fn(x) is in units of
-    2^scale_log (half-step outputs: scale_log = DLOG - 1)."""
-    tab = [0] * 16
-    for x in range(w0, w0 + 16):
-        xm, v = x % 32, _u64(int(fn(x)) << scale_log)
-        if xm < 16:
-            tab[xm] = v
-        else:
-            tab[xm - 16] = _u64(-v)
-    return np.array(tab, dtype=np.uint64)
-
-
 class Context:
     """Keys of both parameter sets and the cross-parameter keyswitching keys."""
 
@@ -66,37 +48,8 @@ class Context:
         self.ksk_ab, self.pab, self.ksk_ba, self.pba = ksk_ab, pab, ksk_ba, pba
         self.dev = device
         self.dim = PA.k * PA.N
-        self.pbs_count = 0
-        self._lut_cache = {}
 
-    # ---------------------------------------------------------- primitives
-    def luts(self, tables):
-        key = tuple(t.tobytes() for t in tables)
-        if key not in self._lut_cache:
-            self._lut_cache[key] = sz.build_testpoly(wl.to_dev(np.stack(tables), self.dev), 4, self.PA.N)
-        return self._lut_cache[key]
-
-    def pbs(self, ct, tables, ids=None):
-        """PBS of every row of ct [count][dim+1] with tables[ids[i]]."""
-        ct = ct.reshape(-1, self.dim + 1).contiguous()
-        if ids is not None:
-            ids = torch.as_tensor(np.asarray(ids, np.int32), device=self.dev)
-        self.pbs_count += ct.shape[0]
-        return sz.pbs_batch(ct, ids, self.luts(tables), self.ka["fbsk"], self.ka["ksk"], self.PA)
-
-    def lin(self, terms, cst: int = 0):
-        """sum_t coef_t ct_t + cst (elementwise over rows) by one linear kernel."""
-        cts = [c.reshape(-1, self.dim + 1) for _, c in terms]
-        count = cts[0].shape[0]
-        stacked = torch.cat(cts, 0).contiguous()
-        T = len(terms)
-        idx = (torch.arange(T, dtype=torch.int64, device=self.dev)[None, :] * count
-               + torch.arange(count, dtype=torch.int64, device=self.dev)[:, None]).to(torch.int32)
-        coef = torch.tensor([int(c) for c, _ in terms], dtype=torch.int64, device=self.dev).repeat(count, 1)
-        cst_t = torch.full((count,), np.int64(np.uint64(_u64(cst)).view(np.int64)), dtype=torch.int64,
-                           device=self.dev)
-        return sz.lwe_linear_batch(stacked, idx.contiguous(), coef.contiguous(), cst_t)
-
+    # ------------------------------------------------------------- helpers
     def decrypt(self, ct, signed_mod: int = 32):
         """Test/diagnostic helper: decode every row (set-A big key)."""
         ph = wl.to_host_u64(sz.lwe_phase_batch(ct.reshape(-1, self.dim + 1).contiguous(), self.ka["big_key"]))
@@ -113,14 +66,8 @@ class Context:
         return res
 
     def channel16(self, z):
-        """r at 2^60 (r in [0, 16), the native mod-16 channel) -> r at Delta.
-        z reads index 2r of Z_32; s' = PBS(z; -4) is -4 for r < 8 and +4 for
-        r >= 8 (negacyclic), x = z - 2 s' - 8 = 2 (r mod 8), and
-        r = PBS(x; x/2 + 4) + s' (toolbox T4 with e = [r >= 8])."""
-        sp = self.pbs(z, [table16(lambda x: -4, 0)])
-        x = self.lin([(1, z), (-2, sp)], cst=-8 << DLOG)
-        hi = self.pbs(x, [table16(lambda v: v // 2 + 4, 0)])
-        return self.lin([(1, hi), (1, sp)])
+        """r at 2^60 (the native mod-16 channel) -> r at Delta (silenzio_channel16)."""
+        return sz.channel16(z, self.ka["fbsk"], self.ka["ksk"], self.PA)
 
     def shift2msbs(self, res, base, times=None):
         """Shift2MSBs+- (Alg. 4) to Gamma = 4: residues [k][count] -> [count] in [-7, 7]."""
@@ -140,40 +87,19 @@ class Context:
         return Y
 
     def sign3(self, res, base):
-        """Sign^RNS_(-1,0,1): [count] in {-1, 0, 1} at Delta."""
-        ka = self.ka
-        digits = sz.rns2mrns(res, base, ka["fbsk"], ka["ksk"], self.PA)
-        k = len(base)
-        nz = [self.pbs(digits[i], [table16(lambda v: 1 if v else 0, 0)]) for i in range(k)]
-        top = base[-1] // 2
-        e = self.pbs(digits[k - 1], [table16(lambda v: 8 if v >= top else 0, 0)])
-        packed = self.lin([(1, t) for t in nz] + [(1, e)])        # sum of [d != 0] + 8 [neg], in [0, 14]
-        return self.pbs(packed, [table16(lambda v: 0 if v % 8 == 0 else (-1 if v >= 8 else 1), 0)])
+        """Sign^RNS_(-1,0,1): [count] in {-1, 0, 1} at Delta (silenzio_rns_sign3)."""
+        return sz.rns_sign3(res, base, self.ka["fbsk"], self.ka["ksk"], self.PA)
 
     def relu_cap(self, S, cap: int):
-        return self.pbs(S, [table16(lambda v: min(max(v, 0), cap), -8)])
+        return sz.relu_cap(S, cap, self.ka["fbsk"], self.ka["ksk"], self.PA)
 
     def relu_mask(self, E, S, cap: int):
         """E in {-1, 0, 1} times the ReLU_x derivative [0 < S < cap] (R25)."""
-        m4 = self.pbs(S, [table16(lambda v: 4 if 0 < v < cap else 0, -8)])
-        packed = self.lin([(1, E), (1, m4)], cst=1 << DLOG)      # (E + 1) + 4 [mask], in [0, 6]
-        return self.pbs(packed, [table16(lambda v: v - 5 if v >= 4 else 0, 0)])
+        return sz.relu_mask(E, S, cap, self.ka["fbsk"], self.ka["ksk"], self.PA)
 
     def update(self, W, G, wmin: int = -8, wmax: int = 7):
-        """clip(W - G) for W in [wmin, wmax], G in {-1, 0, 1}:
-        W - G + [W = wmin][G = 1] - [W = wmax][G = -1] written as
-        W - e+ [W != wmin] + e- [W != wmax], each product a bit x 4-bit T4:
-        f(e, W) = PBS(W; (g0 + g1)/2) + PBS(16 e + W; (g0 - g1)/2) (half steps),
-        then a refreshing identity PBS (fresh noise for the next step)."""
-        ep = self.pbs(G, [table16(lambda g: 1 if g == 1 else 0, -8)])
-        em = self.pbs(G, [table16(lambda g: 1 if g == -1 else 0, -8)])
-        h = DLOG - 1
-        A1 = self.pbs(W, [table16(lambda v: -(v != wmin), -8, h)])
-        B1 = self.pbs(self.lin([(16, ep), (1, W)]), [table16(lambda v: (v != wmin), -8, h)])
-        A2 = self.pbs(W, [table16(lambda v: (v != wmax), -8, h)])
-        B2 = self.pbs(self.lin([(16, em), (1, W)]), [table16(lambda v: -(v != wmax), -8, h)])
-        s = self.lin([(1, W), (1, A1), (1, B1), (1, A2), (1, B2)])
-        return self.pbs(s, [table16(lambda v: v, -8)])
+        """clip(W - G) for G in {-1, 0, 1} (silenzio_weight_update)."""
+        return sz.weight_update(W, G, wmin, wmax, self.ka["fbsk"], self.ka["ksk"], self.PA)
 
     # ------------------------------------------------------- one training step
     def _tick(self, times, name):

@@ -97,8 +97,7 @@ def test_train_step_paper_shaped_mlp(dev):
     check(ctx, newW, it, refW, ref)
     rep["stage_s"] = it["times"]
     rep.update({"workload": "Alg. 6 training step, MLP 28-8-2, batch 8, set A + set-B Shift2MSBs stage",
-                "weights_changed": [int((r != W0).sum()) for r, W0 in zip(refW, ref["W_in"])],
-                "pbs_set_a_outside_drivers": ctx.pbs_count})
+                "weights_changed": [int((r != W0).sum()) for r, W0 in zip(refW, ref["W_in"])]})
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/train_step.json", "w") as f:
         json.dump(rep, f)
