@@ -339,3 +339,50 @@ def digit_combine_fhe(ctx: Ctx, cb: CtxB, top_digit, abs_digits, maxes, top_radi
     for i in range(1, k):
         out = axpy([(1, out), (1, R[i])])
     return out, mb
+
+
+# ------------------------------------------------- training-step gadgets
+# Schedules of DESIGN.md §6b'' (R23-R26), written independently of
+# paper_2504_17785_b200/csrc/gadgets_train.cu with oracle PBS / numpy u64 only.
+def channel16_fhe(ctx: Ctx, z):
+    """Residue r in [0, 16) at 2^60 -> r at Delta: s' = PBS(z; -4) (index 2r,
+    negacyclic), x = z - 2 s' - 8, r = PBS(x; x/2 + 4) + s'."""
+    sp = ctx.lut(z, [table(0, lambda x: -4, DELTA_LOG)])
+    x = axpy([(1, z), (-2, sp)], -(8 << DELTA_LOG))
+    hi = ctx.lut(x, [table(0, lambda v: v // 2 + 4, DELTA_LOG)])
+    return axpy([(1, hi), (1, sp)])
+
+
+def sign3_fhe(ctx: Ctx, res, moduli):
+    """Sign^RNS_(-1,0,1): MRNS digits, [d_i != 0] per digit and
+    8 [top >= 8] summed, one PBS: 0 if no digit is nonzero, -1 / +1 by the sign."""
+    digits = rns2mrns_fhe(ctx, res, moduli)
+    top = moduli[-1] // 2
+    terms = [(1, ctx.lut(d, [table(0, lambda v: 1 if v else 0, DELTA_LOG)])) for d in digits]
+    terms.append((1, ctx.lut(digits[-1], [table(0, lambda v: 8 if v >= top else 0, DELTA_LOG)])))
+    packed = axpy(terms)
+    return ctx.lut(packed, [table(0, lambda v: 0 if v % 8 == 0 else (-1 if v >= 8 else 1), DELTA_LOG)])
+
+
+def relu_cap_fhe(ctx: Ctx, x, cap: int):
+    return ctx.lut(x, [table(-8, lambda v: min(max(v, 0), cap), DELTA_LOG)])
+
+
+def relu_mask_fhe(ctx: Ctx, e, s, cap: int):
+    """e in {-1, 0, 1} times [0 < s < cap]: packed (e + 1) + 4 [mask], one PBS."""
+    m4 = ctx.lut(s, [table(-8, lambda v: 4 if 0 < v < cap else 0, DELTA_LOG)])
+    packed = axpy([(1, e), (1, m4)], 1 << DELTA_LOG)
+    return ctx.lut(packed, [table(0, lambda v: v - 5 if v >= 4 else 0, DELTA_LOG)])
+
+
+def weight_update_fhe(ctx: Ctx, w, g, wmin: int = -8, wmax: int = 7):
+    """clip(w - g) = w - e+ [w != wmin] + e- [w != wmax], e+- = [g = +-1], each
+    product by toolbox T4 (half-step tables), then an identity refresh."""
+    ep = ctx.lut(g, [table(-8, lambda v: 1 if v == 1 else 0, DELTA_LOG)])
+    em = ctx.lut(g, [table(-8, lambda v: 1 if v == -1 else 0, DELTA_LOG)])
+    a1 = ctx.lut(w, [table_raw(-8, lambda v: -(v != wmin) * HALF_DELTA)])
+    b1 = ctx.lut(axpy([(16, ep), (1, w)]), [table_raw(-8, lambda v: (v != wmin) * HALF_DELTA)])
+    a2 = ctx.lut(w, [table_raw(-8, lambda v: (v != wmax) * HALF_DELTA)])
+    b2 = ctx.lut(axpy([(16, em), (1, w)]), [table_raw(-8, lambda v: -(v != wmax) * HALF_DELTA)])
+    s = axpy([(1, w), (1, a1), (1, b1), (1, a2), (1, b2)])
+    return ctx.lut(s, [table(-8, lambda v: v, DELTA_LOG)])

@@ -104,3 +104,35 @@ def test_int_ce_grad_fhe_tiny():
     out = F.int_ce_grad_fhe(ctx, encrypt_ints(P, K, Yhat, 1), encrypt_ints(P, K, Y, 2))
     got = G.signed_decode(oracle.decode(oracle.lwe_phase(out, K["big_key"]), P.p), 32)
     assert np.array_equal(got, G.int_ce_loss_deriv(Yhat, Y, gamma=3, kappa=0))
+
+
+def test_training_gadget_compositions_decrypt_to_their_functions():
+    """oracle.fhe_gadgets training-step compositions (DESIGN.md §6b'') against
+    their cleartext definitions at small n: channel16 (every r at 2^60),
+    ReLU_x, the ReLU_x-derivative mask, the clipped update and Sign^RNS_(-1,0,1)
+    (np.sign of the CRT value)."""
+    P = get_params("A_SMALLN")
+    K = oracle.keygen(P, key_randomness(P, 37))
+    ctx = F.Ctx(P, K)
+    key = K["big_key"]
+
+    def enc(vals, seed, scale_log=59):
+        vals = np.asarray(vals, dtype=np.int64).reshape(-1)
+        r = lwe_randomness(P, vals.size, seed)
+        pt = (vals % (1 << (64 - scale_log))).astype(np.uint64) << np.uint64(scale_log)
+        return oracle.lwe_encrypt(pt, key, r["mask"], r["noise"])
+
+    dec = lambda ct: G.signed_decode(oracle.lwe_decrypt(ct, key, 4), 32)  # noqa: E731
+    r = np.array([0, 5, 7, 8, 9, 15])
+    assert np.array_equal(dec(F.channel16_fhe(ctx, enc(r, 1, 60))), r)
+    x = np.array([-8, -1, 0, 3, 6, 7])
+    assert np.array_equal(dec(F.relu_cap_fhe(ctx, enc(x, 2), 6)), np.clip(x, 0, 6))
+    e, s = np.array([-1, 1, 1, 0, -1, 1]), np.array([3, 0, 7, 2, -4, 6])
+    assert np.array_equal(dec(F.relu_mask_fhe(ctx, enc(e, 3), enc(s, 4), 7)), e * ((s > 0) & (s < 7)))
+    w, g = np.array([-8, -8, 7, 7, 0, 3]), np.array([1, -1, -1, 1, 0, -1])
+    assert np.array_equal(dec(F.weight_update_fhe(ctx, enc(w, 5), enc(g, 6))), np.clip(w - g, -8, 7))
+    base = [13, 16]
+    v = np.array([0, 1, -1, 103, -104, 57])
+    res = G.to_rns(v, base)
+    rc = np.stack([enc(res[i], 10 + i) for i in range(len(base))])
+    assert np.array_equal(dec(F.sign3_fhe(ctx, rc, base)), np.sign(v))
