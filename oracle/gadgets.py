@@ -271,3 +271,43 @@ def train_step(A0, Y, Ws, Gamma: int = 4, w: int = 4, cap: int = 7, wmin: int = 
         newW[l] = np.clip(W - G, wmin, wmax)
     return newW, {"pre": pre, "acts": acts, "Z": Z, "errs": errs, "grads": grads, "bases": bases_f,
                   "W_in": [np.asarray(W, dtype=np.int64) for W in Ws]}
+
+
+# ------------------------------------------- Alg. 7 MatmulHighRes^RNS (NEXT #2)
+BASES5 = [(31, 30), (29, 31, 30), (27, 29, 31, 28), (25, 27, 29, 31, 28), (23, 25, 27, 29, 31, 28)]
+
+
+def extract_bits(x, lo: int, hi: int):
+    """extractBits(x, [lo, hi]): the integer formed by bits lo..hi of x >= 0."""
+    return (np.asarray(x, dtype=np.int64) >> lo) & ((1 << (hi - lo + 1)) - 1)
+
+
+def matmul_highres_rns(X, W, moduli, block: int = 7):
+    """Alg. 7 MatmulHighRes^RNS in cleartext, steps in the paper's order:
+    1. X' = X mod m, W' = W mod m (k x a x b, k x b x c);
+    2. X2' = extractBits(X', [3, 4]), X1' = extractBits(X', [0, 2]);
+    3. Y1* = X1' W' mod m (k x a x b x c); Y2* = X2' W'; Y2* = lookupComp(Y2* 8 mod m)
+       (R15: the expandDims of step 3 take X1' and X2');
+    4. Y* = Y1* + Y2* mod m;
+    5. block-wise summation with n = min(7, b), as Alg. 2's step 3."""
+    X = np.asarray(X, dtype=np.int64)
+    W = np.asarray(W, dtype=np.int64)
+    m = np.asarray(moduli, dtype=np.int64).reshape(-1, 1, 1)
+    Xp = np.mod(X[None], m)
+    Wp = np.mod(W[None], m)
+    X2 = extract_bits(Xp, 3, 4)
+    X1 = extract_bits(Xp, 0, 2)
+    m4 = m[..., None]
+    Y1 = np.mod(X1[:, :, :, None] * Wp[:, None, :, :], m4)
+    Y2 = X2[:, :, :, None] * Wp[:, None, :, :]
+    Y2 = np.mod(Y2 * 8, m4)
+    Ys = np.mod(Y1 + Y2, m4)
+    b = X.shape[1]
+    n = min(block, b)
+    Y = np.mod(Ys[:, :, :n, :].sum(axis=2), m)
+    i = n
+    while i < b:
+        j = min(i + n, b)
+        Y = np.mod(Y + Ys[:, :, i:j, :].sum(axis=2), m)
+        i += n
+    return Y

@@ -202,3 +202,24 @@ def test_train_step_pinned_to_plain_integer_math():
         assert M > 2 * bound + 1 and base[-1] == 16
         smaller = [b for b in G.BASES4 if math.prod(b) < M]
         assert all(math.prod(b) <= 2 * bound + 1 for b in smaller)
+
+
+# ------------------------------------------ Alg. 7 MatmulHighRes^RNS (NEXT #2)
+def test_matmul_highres_pinned_to_integer_matmul():
+    """Cleartext Alg. 7 against plain integer math: the chunk identity
+    X' = X1' + 8 X2' for every 5-bit residue, and CRT of the output equals X @ W
+    for 8-bit inputs whenever |X W| < M / 2 (Table rns_bases_5bit)."""
+    import math
+    xs = np.arange(32)
+    assert np.array_equal(G.extract_bits(xs, 0, 2) + 8 * G.extract_bits(xs, 3, 4), xs)
+    rng = np.random.default_rng(11)
+    for (a, b, c), base in (((3, 5, 2), (31, 30)), ((4, 9, 3), (29, 31, 30)), ((2, 20, 4), (27, 29, 31, 28))):
+        M = math.prod(base)
+        lim = 8 if M < 2 * b * 127 * 128 + 1 else 128
+        X = rng.integers(-lim, lim, size=(a, b))
+        W = rng.integers(-lim, lim, size=(b, c))
+        assert 2 * np.abs(X @ W).max() < M
+        Y = G.matmul_highres_rns(X, W, list(base))
+        assert Y.shape == (len(base), a, c)
+        assert np.array_equal(G.signed_decode(G.crt(Y, list(base)), M), X @ W)
+        assert np.array_equal(Y, G.matmul_rns(X, W, list(base)))   # same residues as Alg. 2
