@@ -386,3 +386,37 @@ def weight_update_fhe(ctx: Ctx, w, g, wmin: int = -8, wmax: int = 7):
     b2 = ctx.lut(axpy([(16, em), (1, w)]), [table_raw(-8, lambda v: -(v != wmax) * HALF_DELTA)])
     s = axpy([(1, w), (1, a1), (1, b1), (1, a2), (1, b2)])
     return ctx.lut(s, [table(-8, lambda v: v, DELTA_LOG)])
+
+
+# ---------------------------------------------- Alg. 7 MatmulHighRes (NEXT #2)
+def matmul_highres_fhe(cb: CtxB, X, W, moduli):
+    """Alg. 7 with 8-bit set-B lookups (R27), written
+    independently of paper_2504_17785_b200/highres.py: X [a][b], W [b][c]
+    signed 8-bit ciphertexts at 2^55 (set-A big key) -> residues [k][a][c]."""
+    X, W = np.asarray(X, dtype=np.uint64), np.asarray(W, dtype=np.uint64)
+    a, b, c = X.shape[0], X.shape[1], W.shape[1]
+    sc = lambda v: v << DELTA_B_LOG  # noqa: E731
+    out = []
+    for m in moduli:
+        x1 = cb.lut(X.reshape(a * b, -1), [table_b(-128, lambda x, m=m: sc((x % m) & 7))]).reshape(a, b, -1)
+        x2 = cb.lut(X.reshape(a * b, -1), [table_b(-128, lambda x, m=m: sc((x % m) >> 3))]).reshape(a, b, -1)
+        w8 = cb.lut(W.reshape(b * c, -1), [table_b(-128, lambda x, m=m: sc(8 * (x % m)))]).reshape(b, c, -1)
+        w4 = cb.lut(W.reshape(b * c, -1), [table_b(-128, lambda x, m=m: sc(4 * (x % m)))]).reshape(b, c, -1)
+        res = np.zeros((a, c, X.shape[-1]), dtype=np.uint64)
+        for i in range(a):
+            for j in range(c):
+                terms = []
+                for kk in range(b):
+                    p1 = axpy([(1, w8[kk, j]), (1, x1[i, kk])])
+                    p2 = axpy([(1, w4[kk, j]), (1, x2[i, kk])])
+                    terms.append(cb.lut(p1[None], [table_b(0, lambda v, m=m: sc(((v & 7) * (v >> 3)) % m))])[0])
+                    terms.append(cb.lut(p2[None], [table_b(0, lambda v, m=m: sc((8 * (v & 3) * (v >> 2)) % m))])[0])
+                while len(terms) > 1:
+                    nxt = []
+                    for g in range(0, len(terms), 8):
+                        s = axpy([(1, t) for t in terms[g:g + 8]])
+                        nxt.append(cb.lut(s[None], [table_b(0, lambda v, m=m: sc(v % m))])[0])
+                    terms = nxt
+                res[i, j] = terms[0]
+        out.append(res)
+    return np.stack(out)

@@ -67,3 +67,38 @@ def test_matmul_highres_full_params(dev):
     with open("gpurun_out/highres.json", "w") as f:
         json.dump(rep, f)
     print(json.dumps(rep))
+
+
+def test_matmul_highres_tiny_gpu_vs_oracle_composition(dev):
+    """1x2 . 2x1 with base (31, 30) at small n: the GPU schedule and the oracle's
+    independent composition (oracle/fhe_gadgets.py) on identical ciphertexts
+    agree in phase within 2^-32 on every output residue (same keys: the set-A
+    and set-B keys and both cross keyswitching keys are generated bit-exactly)."""
+    import oracle
+    from oracle import fhe_gadgets as F
+    from paper_2504_17785_b200 import highres as HR, training as TR, workload as wl
+    from synth import cross_ksk_randomness, key_randomness
+    PA, PB = get_params("A_SMALLN"), get_params("B_SMALLN")
+    seed = 143
+    ctx = TR.make_context(PA, PB, seed, dev)
+    oa, ob = oracle.keygen(PA, key_randomness(PA, seed)), oracle.keygen(PB, key_randomness(PB, seed + 1))
+    rab = cross_ksk_randomness(PA.big_dim, 5, PB.n, PB.lwe_sigma_log2, seed, 1)
+    rba = cross_ksk_randomness(PB.big_dim, 4, PA.big_dim, PA.glwe_sigma_log2, seed, 2)
+    cb = F.CtxB(PB, ob, oracle.ksk_generate(oa["big_key"], ob["lwe_key"], rab, 4, 5), (PA.big_dim, PB.n, 4, 5),
+                oracle.ksk_generate(ob["big_key"], oa["big_key"], rba, 10, 4), (PB.big_dim, PA.big_dim, 10, 4))
+    X, W = np.array([[-77, 113]]), np.array([[90], [-128]])
+    def enc(v, s):
+        v = np.asarray(v).reshape(-1)
+        r = lwe_randomness(PA, v.size, s)
+        return oracle.lwe_encrypt((v % 512).astype(np.uint64) << np.uint64(55), oa["big_key"], r["mask"], r["noise"])
+    Xc, Wc = enc(X, 1).reshape(1, 2, -1), enc(W, 2).reshape(2, 1, -1)
+    base = [31, 30]
+    got = HR.HighRes(ctx).matmul(wl.to_dev(Xc, dev), wl.to_dev(Wc, dev), base)
+    got = got.cpu().numpy().view(np.uint64).reshape(len(base), 1, 1, -1)
+    ref = F.matmul_highres_fhe(cb, Xc, Wc, base)
+    key = oa["big_key"]
+    dphi = np.abs(oracle.torus_diff(oracle.lwe_phase(got.reshape(-1, got.shape[-1]), key),
+                                    oracle.lwe_phase(ref.reshape(-1, ref.shape[-1]), key)))
+    assert dphi.max() <= 2 ** 32, int(dphi.max())
+    res = (oracle.lwe_decrypt(got.reshape(-1, got.shape[-1]), key, 8) % 512).reshape(2, 1, 1)
+    assert np.array_equal(res, G.matmul_highres_rns(X, W, base))
