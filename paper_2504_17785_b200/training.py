@@ -57,49 +57,74 @@ class Context:
         return np.where(2 * v >= signed_mod, v - signed_mod, v)
 
     # ------------------------------------------------------------- gadgets
-    def matmul(self, X, W, base):
+    def matmul(self, X, W, base, stream=None):
         """Matmul^RNS (Alg. 2) -> residues [k][a][c] all at Delta (channel16 applied)."""
-        res = sz.rns_matmul(X.contiguous(), W.contiguous(), base, self.ka["fbsk"], self.ka["ksk"], self.PA)
+        res = sz.rns_matmul(X.contiguous(), W.contiguous(), base, self.ka["fbsk"], self.ka["ksk"], self.PA,
+                            stream=stream)
         k, a, c = res.shape[0], res.shape[1], res.shape[2]
         if base[-1] == 16:
-            res[k - 1] = self.channel16(res[k - 1]).reshape(a, c, -1)
+            res[k - 1] = self.channel16(res[k - 1], stream).reshape(a, c, -1)
         return res
 
-    def channel16(self, z):
+    def channel16(self, z, stream=None):
         """r at 2^60 (the native mod-16 channel) -> r at Delta (silenzio_channel16)."""
-        return sz.channel16(z, self.ka["fbsk"], self.ka["ksk"], self.PA)
+        return sz.channel16(z, self.ka["fbsk"], self.ka["ksk"], self.PA, stream=stream)
 
     def shift2msbs(self, res, base, times=None):
         """Shift2MSBs+- (Alg. 4) to Gamma = 4: residues [k][count] -> [count] in [-7, 7]."""
         ka = self.ka
         tick = lambda name: self._tick(times, name)  # noqa: E731
-        digits = sz.rns2mrns(res, base, ka["fbsk"], ka["ksk"], self.PA)
-        tick("s2m rns2mrns")
-        _, absr = sz.rns_sign_abs(res, base, ka["fbsk"], ka["ksk"], self.PA)
-        tick("s2m sign_abs")
-        dabs = sz.rns2mrns(absr, base, ka["fbsk"], ka["ksk"], self.PA)
-        tick("s2m rns2mrns")
-        _, mx = sz.mrns_bitlen_max(dabs, ka["fbsk"], ka["ksk"], self.PA)
-        tick("s2m bitlen_max")
+        # the MRNS digits of x and the |x| -> digits -> block max chain are independent
+        def chain_abs(st):
+            _, absr = sz.rns_sign_abs(res, base, ka["fbsk"], ka["ksk"], self.PA, stream=st)
+            dabs = sz.rns2mrns(absr, base, ka["fbsk"], ka["ksk"], self.PA, stream=st)
+            _, mx = sz.mrns_bitlen_max(dabs, ka["fbsk"], ka["ksk"], self.PA, stream=st)
+            return dabs, mx
+        digits, (dabs, mx) = self._par(lambda st: sz.rns2mrns(res, base, ka["fbsk"], ka["ksk"], self.PA, stream=st),
+                                       chain_abs)
+        tick("s2m rns2mrns | sign_abs, rns2mrns, bitlen_max")
         Y, _ = sz.mrns_digit_combine(digits[-1].contiguous(), dabs, mx, base[-1], W_BITS, 3, ka, self.PA,
                                      self.kb, self.PB, self.ksk_ab, self.pab, self.ksk_ba, self.pba)
         tick("s2m digit_combine (set B)")
         return Y
 
-    def sign3(self, res, base):
+    def sign3(self, res, base, stream=None):
         """Sign^RNS_(-1,0,1): [count] in {-1, 0, 1} at Delta (silenzio_rns_sign3)."""
-        return sz.rns_sign3(res, base, self.ka["fbsk"], self.ka["ksk"], self.PA)
+        return sz.rns_sign3(res, base, self.ka["fbsk"], self.ka["ksk"], self.PA, stream=stream)
 
     def relu_cap(self, S, cap: int):
         return sz.relu_cap(S, cap, self.ka["fbsk"], self.ka["ksk"], self.PA)
 
-    def relu_mask(self, E, S, cap: int):
+    def relu_mask(self, E, S, cap: int, stream=None):
         """E in {-1, 0, 1} times the ReLU_x derivative [0 < S < cap] (R25)."""
-        return sz.relu_mask(E, S, cap, self.ka["fbsk"], self.ka["ksk"], self.PA)
+        return sz.relu_mask(E, S, cap, self.ka["fbsk"], self.ka["ksk"], self.PA, stream=stream)
 
-    def update(self, W, G, wmin: int = -8, wmax: int = 7):
+    def update(self, W, G, wmin: int = -8, wmax: int = 7, stream=None):
         """clip(W - G) for G in {-1, 0, 1} (silenzio_weight_update)."""
-        return sz.weight_update(W, G, wmin, wmax, self.ka["fbsk"], self.ka["ksk"], self.PA)
+        return sz.weight_update(W, G, wmin, wmax, self.ka["fbsk"], self.ka["ksk"], self.PA, stream=stream)
+
+    def _par(self, *fns):
+        """Run independent gadget chains concurrently: each on its own CUDA stream
+        (ordered after the current stream's work) in its own host thread (the
+        drivers block on their stream); the current stream then waits for all."""
+        import concurrent.futures as cf
+        cur = torch.cuda.current_stream(self.dev)
+        streams = [torch.cuda.Stream(device=self.dev) for _ in fns]
+        for st in streams:
+            st.wait_stream(cur)
+
+        def run(f, st):
+            with torch.cuda.stream(st):
+                return f(st)
+        with cf.ThreadPoolExecutor(len(fns)) as ex:
+            outs = [f.result() for f in [ex.submit(run, f, st) for f, st in zip(fns, streams)]]
+        for st in streams:
+            cur.wait_stream(st)
+        for o in outs:
+            for t in (o if isinstance(o, (tuple, list)) else (o,)):
+                if isinstance(t, torch.Tensor):
+                    t.record_stream(cur)
+        return outs
 
     # ------------------------------------------------------- one training step
     def _tick(self, times, name):
@@ -138,22 +163,30 @@ class Context:
             W = Ws[l]
             c_l, b_l = W.shape[0], W.shape[1]
             gbase = get_rns_base(a * 8)
-            Gm = self.matmul(E.transpose(0, 1), acts[l], gbase)
-            tick("backward matmul")
-            G = self.sign3(Gm.reshape(len(gbase), c_l * b_l, -1), gbase).reshape(c_l, b_l, -1)
-            tick("sign3")
-            if l > 0:
+            Ecur = E
+
+            # gradient branch (G_l, then the weight update) and error branch
+            # (E_{l-1}) only read E, W_l and the activations: run them concurrently
+            def grad_branch(st, W=W, c_l=c_l, b_l=b_l, l=l, Ecur=Ecur):
+                Gm = self.matmul(Ecur.transpose(0, 1), acts[l], gbase, st)
+                G = self.sign3(Gm.reshape(len(gbase), c_l * b_l, -1), gbase, st).reshape(c_l, b_l, -1)
+                nw = self.update(W.reshape(c_l * b_l, -1), G.reshape(c_l * b_l, -1), stream=st)
+                return G, nw.reshape(c_l, b_l, -1)
+
+            def err_branch(st, W=W, c_l=c_l, b_l=b_l, l=l, Ecur=Ecur):
                 ebase = get_rns_base(c_l * 8)
-                Em = self.matmul(E, W, ebase)
-                tick("backward matmul")
-                En = self.sign3(Em.reshape(len(ebase), a * b_l, -1), ebase)
-                tick("sign3")
-                E = self.relu_mask(En, pre[l - 1].reshape(a * b_l, -1), cap).reshape(a, b_l, -1)
-                tick("relu")
+                Em = self.matmul(Ecur, W, ebase, st)
+                En = self.sign3(Em.reshape(len(ebase), a * b_l, -1), ebase, st)
+                return self.relu_mask(En, pre[l - 1].reshape(a * b_l, -1), cap, st).reshape(a, b_l, -1)
+
+            if l > 0:
+                (G, nw), E = self._par(grad_branch, err_branch)
                 inter["errs"].append(E)
+            else:
+                G, nw = grad_branch(None)
             inter["grads"].insert(0, G)
-            newW[l] = self.update(W.reshape(c_l * b_l, -1), G.reshape(c_l * b_l, -1)).reshape(c_l, b_l, -1)
-            tick("update")
+            newW[l] = nw
+            tick("backward (gradient | error branches) + update")
         inter["pre"], inter["acts"] = pre, acts
         if times is not None:
             times.pop("_t")
