@@ -62,3 +62,23 @@ def test_host_side_sizing_and_validation(lib):
     rc = L.silenzio_pbs_batch(None, None, None, 1, None, None, None, 5, ctypes.byref(silenzio.make_params(P)), None, None)
     assert rc == -3
     assert L.silenzio_status_string(-7) == b"CUDA error"
+
+
+def test_training_gadget_validation_without_gpu(lib):
+    """Host-side validation of the training-step and gadget entry points: bad
+    shapes / windows / null pointers are reported before any launch."""
+    from paper_2504_17785_b200 import silenzio
+    from synth import get_params
+    L = silenzio.load()
+    P = silenzio.make_params(get_params("A"))
+    fake = ctypes.c_void_p(256)
+    big_ws = ctypes.c_size_t(1 << 62)
+    mods = (ctypes.c_uint32 * 3)(11, 13, 15)          # top modulus must be 16 for sign3
+    assert L.silenzio_rns_sign3(fake, mods, 3, 4, fake, fake, fake, ctypes.byref(P), fake, big_ws, None) == -6
+    mods8 = (ctypes.c_uint32 * 8)(*([5] * 7 + [16]))  # k = 8 > 7: the packed sum would leave the window
+    assert L.silenzio_rns_sign3(fake, mods8, 8, 4, fake, fake, fake, ctypes.byref(P), fake, big_ws, None) == -6
+    assert L.silenzio_relu_cap(fake, 4, 9, fake, fake, fake, ctypes.byref(P), fake, big_ws, None) == -6
+    assert L.silenzio_weight_update(fake, fake, 4, 3, 2, fake, fake, fake, ctypes.byref(P), fake, big_ws, None) == -6
+    assert L.silenzio_channel16(None, 4, fake, fake, fake, ctypes.byref(P), fake, big_ws, None) == -3
+    assert L.silenzio_relu_mask(fake, fake, 4, 7, fake, fake, fake, ctypes.byref(P), None, big_ws, None) == -8
+    assert L.silenzio_train_workspace_bytes(ctypes.byref(P), 6, 100) > L.silenzio_train_workspace_bytes(ctypes.byref(P), 1, 100)
