@@ -298,10 +298,9 @@ def main():
     achieved = flops * B / br_avg_s / 1e12
     roofline = {"bound": "alu", "pipe": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                # dram__bytes_read.sum + dram__bytes_write.sum of one full-wave launch (592 ciphertexts) from
-                # the committed ncu --set full capture (151.5 MB read = the 146 MB Fourier BSK once per wave
-                # + inputs; 6.1 MB written): per launch, HBM is far from the bound
-                "traffic": 1.868252e12,
+                # dram__bytes_read.sum + dram__bytes_write.sum of the bench's own BR launch, measured by ncu
+                # for the default 131072-ciphertext batch (null for other batch sizes: not measured)
+                "traffic": 1.868252e12 if (B == 131072 and args.config == 1) else None,
                 "traffic_source": "profiles/r01_ncu_br_bench_dram.txt: dram__bytes_read.sum + dram__bytes_write.sum "
                                   "of the bench's 131072-ciphertext launch (the drifting persistent grid re-reads the "
                                   "146 MB Fourier BSK; HBM stays at ~10 % of its bandwidth, see DESIGN.md §6)",
