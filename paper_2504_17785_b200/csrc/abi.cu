@@ -194,6 +194,7 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
   if (P->ks_in_dim != P->glwe_dim * P->poly_size) return SILENZIO_ERR_INVALID_PARAM;
   if (count == 0) return SILENZIO_OK;
   if (!in || !luts || !fbsk || !ksk || !out) return SILENZIO_ERR_NULL_POINTER;
+  if (count > (1ull << 31)) return SILENZIO_ERR_COUNT;  // the blind rotation's limit, checked before the keyswitch runs
   if (!workspace) return SILENZIO_ERR_WORKSPACE;
   if (in == out) return SILENZIO_ERR_INVALID_PARAM;
   if (!sz_aligned16(workspace)) return SILENZIO_ERR_MISALIGNED;

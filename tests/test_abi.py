@@ -82,3 +82,18 @@ def test_training_gadget_validation_without_gpu(lib):
     assert L.silenzio_channel16(None, 4, fake, fake, fake, ctypes.byref(P), fake, big_ws, None) == -3
     assert L.silenzio_relu_mask(fake, fake, 4, 7, fake, fake, fake, ctypes.byref(P), None, big_ws, None) == -8
     assert L.silenzio_train_workspace_bytes(ctypes.byref(P), 6, 100) > L.silenzio_train_workspace_bytes(ctypes.byref(P), 1, 100)
+
+
+def test_maximum_count_is_rejected_before_any_launch(lib):
+    """count above the blind rotation's 2^31 limit is reported (SILENZIO_ERR_COUNT)
+    by silenzio_pbs_batch and silenzio_blind_rotate_batch before anything runs."""
+    from paper_2504_17785_b200 import silenzio
+    from synth import get_params
+    L = silenzio.load()
+    P = silenzio.make_params(get_params("A"))
+    fake = ctypes.c_void_p(256)
+    n = (1 << 31) + 1
+    assert L.silenzio_pbs_batch(fake, None, fake, 1, fake, fake, ctypes.c_void_p(512), n, ctypes.byref(P), fake,
+                                None) == -5
+    assert L.silenzio_blind_rotate_batch(fake, None, fake, 1, fake, ctypes.c_void_p(512), n, ctypes.byref(P), None,
+                                         None) == -5
