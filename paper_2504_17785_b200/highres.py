@@ -66,7 +66,7 @@ class HighRes:
         """Cross-parameter keyswitch (kp: silenzio_params of the keyswitch)."""
         out = torch.empty((ct.shape[0], kp.lwe_dim + 1), dtype=torch.int64, device=self.c.dev)
         sz._check(sz.load().silenzio_keyswitch_batch(sz._ptr(ct.contiguous()), sz._ptr(ksk), sz._ptr(out),
-                                                     ct.shape[0], ctypes.byref(kp), None, None))
+                                                     ct.shape[0], ctypes.byref(kp), None, sz._stream(None)))
         return out
 
     def lin(self, src, idx, coef, cst=None):
@@ -87,8 +87,7 @@ class HighRes:
         nX, nW = a * b, b * cc
         Xf = X.reshape(nX, -1)
         Wf = W.reshape(nW, -1)
-        outs = []
-        for m in moduli:
+        def channel(m):   # one RNS channel (independent of the others)
             # step 1: chunks of X' = X mod m, and W' at 8 Delta_B / 4 Delta_B
             x12 = self.pbs_b(torch.cat([Xf, Xf]), [table256(lambda x, m=m: (x % m) & 7, -128),
                                                    table256(lambda x, m=m: (x % m) >> 3, -128)],
@@ -125,5 +124,6 @@ class HighRes:
                 s = self.lin(cur, idx, coef)
                 cur = self.pbs_b(s, [table256(lambda v, m=m: v % m, 0)])
                 terms = groups
-            outs.append(cur.reshape(a, cc, -1))
-        return torch.stack(outs)
+            return cur.reshape(a, cc, -1)
+        # the channels run concurrently, each on its own stream (training.Context._par)
+        return torch.stack(self.c._par(*[(lambda st, m=m: channel(m)) for m in moduli]))

@@ -58,13 +58,25 @@ class Context:
 
     # ------------------------------------------------------------- gadgets
     def matmul(self, X, W, base, stream=None):
-        """Matmul^RNS (Alg. 2) -> residues [k][a][c] all at Delta (channel16 applied)."""
-        res = sz.rns_matmul(X.contiguous(), W.contiguous(), base, self.ka["fbsk"], self.ka["ksk"], self.PA,
-                            stream=stream)
-        k, a, c = res.shape[0], res.shape[1], res.shape[2]
-        if base[-1] == 16:
-            res[k - 1] = self.channel16(res[k - 1], stream).reshape(a, c, -1)
-        return res
+        """Matmul^RNS (Alg. 2) -> residues [k][a][c] all at Delta (channel16 applied).
+        The RNS channels are independent: each modulus runs as its own driver
+        call on its own stream, concurrently (a small matmul is a chain of
+        latency-bound PBS launches, so the channels overlap instead of queueing)."""
+        X, W = X.contiguous(), W.contiguous()
+
+        def one(m):
+            def f(st):
+                r = sz.rns_matmul(X, W, [m], self.ka["fbsk"], self.ka["ksk"], self.PA, stream=st)[0]
+                if m == 16:
+                    r = self.channel16(r, st).reshape(r.shape)
+                return r
+            return f
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                chans = self._par(*[one(m) for m in base])
+        else:
+            chans = self._par(*[one(m) for m in base])
+        return torch.stack(chans)
 
     def channel16(self, z, stream=None):
         """r at 2^60 (the native mod-16 channel) -> r at Delta (silenzio_channel16)."""
