@@ -267,6 +267,28 @@ def test_pbs_noiseless_exact_gadget_is_exact():
     assert (ph == T[m]).all()
 
 
+@pytest.mark.parametrize("name,cnt", [("EXACT2048", 4), ("EXACT8192", 2), ("EXACT32768", 1)])
+def test_pbs_noiseless_exact_gadget_is_exact_at_larger_n(name, cnt):
+    """The exact-gadget identity of the test above at the polynomial sizes of
+    parameter sets A (N = 2048, p = 4), C (N = 8192, p = 6) and B: the oracle's
+    schoolbook blind rotation, key layout and sample extraction hold at those N
+    and B (N = 32768, p = 8) (output phase = T[m] bit-exactly, random masks;
+    padding-half inputs -T)."""
+    P = get_params(name)
+    K = oracle.keygen(P, key_randomness(P, 5))
+    tab = [(5 * x + 3) % (1 << P.p) for x in range(1 << P.p)]
+    T = oracle.encode(np.array(tab), P.p + 1)
+    v = oracle.test_polynomial(T, P.p, P.N)
+    m = np.array([(1 << P.p) + 3, 0, (1 << P.p) - 1, 7][:cnt])
+    rnd = lwe_randomness(P, cnt, 5)
+    ct = oracle.lwe_encrypt(oracle.encode(m, P.p), K["big_key"], rnd["mask"], rnd["noise"])
+    out = oracle.pbs(ct, np.zeros(cnt, np.uint32), v, K["bsk"], K["ksk"], P)
+    ph = oracle.lwe_phase(out, K["big_key"])
+    half = 1 << P.p
+    want = np.array([T[x] if x < half else (~T[x - half]) + np.uint64(1) for x in m], dtype=np.uint64)
+    assert (ph == want).all()
+
+
 def test_pbs_correct_and_noise_matches_closed_form():
     P = get_params("TOY")
     K = oracle.keygen(P, key_randomness(P, 5))
