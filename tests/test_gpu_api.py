@@ -1,0 +1,58 @@
+"""GPU checks of the remaining public entry points: the linear LWE kernel
+ against the oracle bit-exactly, and the host-buffer PBS
+(silenzio_pbs_batch_host, the e2e API bench.py times) against the device PBS
+bit-exactly, with a chunk size that does not divide the batch."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from synth import get_params, key_randomness, lut_ids, lut_tables, lwe_randomness, messages
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    return torch.device("cuda:0")
+
+
+def test_lwe_linear_batch_bitexact(dev):
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    rng = np.random.default_rng(161)
+    dim, n_in, count, terms = 2048, 37, 101, 5
+    ct = rng.integers(0, 2 ** 64 - 1, size=(n_in, dim + 1), dtype=np.uint64)
+    idx = rng.integers(0, n_in, size=(count, terms)).astype(np.uint32)
+    coef = rng.integers(-2 ** 40, 2 ** 40, size=(count, terms)).astype(np.int64)
+    coef[0] = [2 ** 63 - 1, -2 ** 63, 0, 1, -1]                      # extremes wrap mod 2^64
+    cst = rng.integers(0, 2 ** 64 - 1, size=count, dtype=np.uint64)
+    got = silenzio.lwe_linear_batch(wl.to_dev(ct, dev), wl.to_dev(idx.view(np.int32), dev),
+                                    wl.to_dev(coef, dev), wl.to_dev(cst, dev))
+    ref = oracle.lwe_linear(ct, idx, coef, cst)
+    assert np.array_equal(wl.to_host_u64(got), ref)
+
+
+def test_pbs_batch_host_equals_device_path(dev):
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P = get_params("A_SMALLN")
+    keys = wl.device_keys(P, key_randomness(P, 162), dev)
+    B, chunk = 1000, 384                                              # ragged last chunk
+    tabs = lut_tables(8, P.p, 162)
+    luts = wl.luts_from_tables(tabs, P.p, P.N, dev)
+    ids = lut_ids(B, 8, 163)
+    m = messages(B, P.p, 163)
+    ct = wl.encrypt(P, m, lwe_randomness(P, B, 163), keys["big_key"], dev)
+    ids_d = torch.from_numpy(ids.astype(np.int32)).to(dev)
+    out_d = silenzio.pbs_batch(ct, ids_d, luts, keys["fbsk"], keys["ksk"], P)
+    ct_h = torch.empty(ct.shape, dtype=torch.int64, pin_memory=True)
+    ct_h.copy_(ct)
+    ids_h = ids_d.cpu().pin_memory()
+    out_h = torch.empty(out_d.shape, dtype=torch.int64, pin_memory=True)
+    ws = torch.empty(silenzio.pbs_host_workspace_bytes(P, chunk), dtype=torch.uint8, device=dev)
+    silenzio.pbs_batch_host(ct_h, ids_h, luts, keys["fbsk"], keys["ksk"], P, out_h, ws, chunk=chunk)
+    torch.cuda.synchronize()
+    assert torch.equal(out_h, out_d.cpu())
+    dec = wl.decode(wl.to_host_u64(silenzio.lwe_phase_batch(out_d, keys["big_key"])), P.p)
+    assert np.array_equal(dec, tabs[ids, m])
