@@ -56,3 +56,23 @@ def test_pbs_batch_host_equals_device_path(dev):
     assert torch.equal(out_h, out_d.cpu())
     dec = wl.decode(wl.to_host_u64(silenzio.lwe_phase_batch(out_d, keys["big_key"])), P.p)
     assert np.array_equal(dec, tabs[ids, m])
+
+
+@pytest.mark.parametrize("limbs,bits", [(1, 22), (2, 43)])
+def test_pbs_fewer_fft_limbs_still_decrypt(limbs, bits, dev):
+    """The P = 1 / 2 limb variants of the blind rotation (speed experiments,
+    DESIGN.md R20: not phase-exact) still decrypt every output correctly and stay
+    within the noise budget; P = 2 keeps the phase within 2^-32 of the oracle on
+    average-case inputs only, so only decryption is asserted here."""
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P = get_params("A_SMALLN", fft_limbs=limbs, limb_bits=bits)
+    keys = wl.device_keys(P, key_randomness(P, 164), dev)
+    B = 600
+    tabs = lut_tables(8, P.p, 164)
+    luts = wl.luts_from_tables(tabs, P.p, P.N, dev)
+    ids = lut_ids(B, 8, 165)
+    m = messages(B, P.p, 165)
+    ct = wl.encrypt(P, m, lwe_randomness(P, B, 165), keys["big_key"], dev)
+    out = silenzio.pbs_batch(ct, torch.from_numpy(ids.astype(np.int32)).to(dev), luts, keys["fbsk"], keys["ksk"], P)
+    dec = wl.decode(wl.to_host_u64(silenzio.lwe_phase_batch(out, keys["big_key"])), P.p)
+    assert np.array_equal(dec, tabs[ids, m])
