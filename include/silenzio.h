@@ -234,6 +234,25 @@ int silenzio_mrns_digit_combine(const uint64_t *top_digit, const uint64_t *abs_d
                                 const uint64_t *ksk_ab, const silenzio_params *pab, const uint64_t *ksk_ba,
                                 const silenzio_params *pba, void *workspace, size_t workspace_bytes, void *stream);
 
+/* Shift2MSBs+- (Alg. 4, l.408-423, over Alg. 3 Shift2MSBs+,
+ * l.337-374) in one call: residues [k][count] at Delta (set A, moduli
+ * ascending, top modulus even) -> out [count] = Shift2MSBs+-(x) in
+ * [-(2^gamma - 1), 2^gamma - 1] at Delta, maxbit_out [1] as in
+ * silenzio_mrns_digit_combine (w = modulus bit width, gamma = Gamma - 1).
+ * Composes RNS2MRNS, sign / abs, RNS2MRNS of |x|, bit lengths + block max and
+ * the 8-bit digit combine (parameters and keys as silenzio_mrns_digit_combine);
+ * the digits-of-x chain and the |x| chain run concurrently on two streams.
+ * workspace >= silenzio_shift2msbs_workspace_bytes(pa, pb, k, count);
+ * synchronises `stream`. */
+size_t silenzio_shift2msbs_workspace_bytes(const silenzio_params *pa, const silenzio_params *pb, uint32_t k,
+                                           size_t count);
+int silenzio_shift2msbs_pm(const uint64_t *residues, const uint32_t *moduli_host, uint32_t k, size_t count,
+                           uint32_t w, uint32_t gamma, uint64_t *out, uint64_t *maxbit_out, const void *fbsk_a,
+                           const uint64_t *ksk_a, const silenzio_params *pa, const void *fbsk_b,
+                           const silenzio_params *pb, const uint64_t *ksk_ab, const silenzio_params *pab,
+                           const uint64_t *ksk_ba, const silenzio_params *pba, void *workspace,
+                           size_t workspace_bytes, void *stream);
+
 /* Training-step gadgets (Alg. 6, l.466-502; SURVEY.md §8(f) NEXT #1;
  * schedules DESIGN.md §6b'', readings R23-R26) at parameter set A. Thin
  * drivers over linear LWE ops and PBS; ciphertext arrays are big-key LWE

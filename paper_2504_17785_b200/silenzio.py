@@ -67,6 +67,8 @@ def load():
         "silenzio_int_ce_grad": ([V, V, U32, U32, V, V, V, P, V, S, V], I),
         "silenzio_mrns_combine_workspace_bytes": ([P, P, U32, S], S),
         "silenzio_mrns_digit_combine": ([V, V, V, U32, S, U32, U32, U32, V, V, V, V, P, V, P, V, P, V, P, V, S, V], I),
+        "silenzio_shift2msbs_workspace_bytes": ([P, P, U32, S], S),
+        "silenzio_shift2msbs_pm": ([V, V, U32, S, U32, U32, V, V, V, V, P, V, P, V, P, V, P, V, S, V], I),
         "silenzio_train_workspace_bytes": ([P, U32, S], S),
         "silenzio_channel16": ([V, S, V, V, V, P, V, S, V], I),
         "silenzio_rns_sign3": ([V, V, U32, S, V, V, V, P, V, S, V], I),
@@ -93,6 +95,7 @@ def exported_symbols():
         "silenzio_rns_matmul", "silenzio_gadget_workspace_bytes", "silenzio_rns2mrns",
         "silenzio_rns_sign_abs", "silenzio_mrns_bitlen_max", "silenzio_int_ce_grad",
         "silenzio_mrns_combine_workspace_bytes", "silenzio_mrns_digit_combine",
+        "silenzio_shift2msbs_workspace_bytes", "silenzio_shift2msbs_pm",
         "silenzio_train_workspace_bytes", "silenzio_channel16", "silenzio_rns_sign3", "silenzio_relu_cap",
         "silenzio_relu_mask", "silenzio_weight_update",
     ]
@@ -440,3 +443,19 @@ def weight_update(w, g, wmin, wmax, fourier_bsk, ksk, P, stream=None):
                                          _ptr(fourier_bsk), _ptr(ksk), ctypes.byref(make_params(P)), _ptr(ws),
                                          ws.numel(), _stream(stream)))
     return out
+
+
+def shift2msbs_pm(residues, moduli, w, gamma, keys_a, Pa, keys_b, Pb, ksk_ab, pab, ksk_ba, pba, stream=None):
+    """Shift2MSBs+- (Alg. 4): residues [k][count] -> (out [count], maxBit [1])."""
+    k, count = int(residues.shape[0]), int(residues.shape[1])
+    res = residues.reshape(k, count, -1).contiguous()
+    out = torch.empty((count, res.shape[-1]), dtype=torch.int64, device=res.device)
+    mb = torch.empty((1, res.shape[-1]), dtype=torch.int64, device=res.device)
+    pa, pb = make_params(Pa), make_params(Pb)
+    nb = load().silenzio_shift2msbs_workspace_bytes(ctypes.byref(pa), ctypes.byref(pb), k, count)
+    ws = torch.empty(nb, dtype=torch.uint8, device=res.device)
+    _check(load().silenzio_shift2msbs_pm(
+        _ptr(res), _moduli(moduli), k, count, w, gamma, _ptr(out), _ptr(mb), _ptr(keys_a["fbsk"]),
+        _ptr(keys_a["ksk"]), ctypes.byref(pa), _ptr(keys_b["fbsk"]), ctypes.byref(pb), _ptr(ksk_ab),
+        ctypes.byref(pab), _ptr(ksk_ba), ctypes.byref(pba), _ptr(ws), ws.numel(), _stream(stream)))
+    return out, mb

@@ -83,21 +83,11 @@ class Context:
         return sz.channel16(z, self.ka["fbsk"], self.ka["ksk"], self.PA, stream=stream)
 
     def shift2msbs(self, res, base, times=None):
-        """Shift2MSBs+- (Alg. 4) to Gamma = 4: residues [k][count] -> [count] in [-7, 7]."""
-        ka = self.ka
-        tick = lambda name: self._tick(times, name)  # noqa: E731
-        # the MRNS digits of x and the |x| -> digits -> block max chain are independent
-        def chain_abs(st):
-            _, absr = sz.rns_sign_abs(res, base, ka["fbsk"], ka["ksk"], self.PA, stream=st)
-            dabs = sz.rns2mrns(absr, base, ka["fbsk"], ka["ksk"], self.PA, stream=st)
-            _, mx = sz.mrns_bitlen_max(dabs, ka["fbsk"], ka["ksk"], self.PA, stream=st)
-            return dabs, mx
-        digits, (dabs, mx) = self._par(lambda st: sz.rns2mrns(res, base, ka["fbsk"], ka["ksk"], self.PA, stream=st),
-                                       chain_abs)
-        tick("s2m rns2mrns | sign_abs, rns2mrns, bitlen_max")
-        Y, _ = sz.mrns_digit_combine(digits[-1].contiguous(), dabs, mx, base[-1], W_BITS, 3, ka, self.PA,
-                                     self.kb, self.PB, self.ksk_ab, self.pab, self.ksk_ba, self.pba)
-        tick("s2m digit_combine (set B)")
+        """Shift2MSBs+- (Alg. 4) to Gamma = 4: residues [k][count] -> [count] in [-7, 7]
+        (silenzio_shift2msbs_pm: the digits-of-x and |x| chains run concurrently)."""
+        Y, _ = sz.shift2msbs_pm(res, base, W_BITS, 3, self.ka, self.PA, self.kb, self.PB,
+                                self.ksk_ab, self.pab, self.ksk_ba, self.pba)
+        self._tick(times, "shift2msbs")
         return Y
 
     def sign3(self, res, base, stream=None):

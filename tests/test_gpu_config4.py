@@ -61,16 +61,12 @@ def gpu_setup(PA, PB, seed, dev, with_oracle):
 
 
 def gpu_shift2msbs(g, res_ct, PA, PB):
-    """Alg. 4 on GPU: sign/abs, MRNS of |x|, bit lengths + block max, 8-bit combine."""
+    """Alg. 4 on GPU in one C-ABI call (silenzio_shift2msbs_pm): sign/abs, MRNS of
+    x and of |x|, bit lengths + block max, 8-bit digit combine."""
     from paper_2504_17785_b200 import silenzio
-    ka = g["ka"]
-    digits = silenzio.rns2mrns(res_ct, BASE6, ka["fbsk"], ka["ksk"], PA)
-    e, absr = silenzio.rns_sign_abs(res_ct, BASE6, ka["fbsk"], ka["ksk"], PA)
-    dabs = silenzio.rns2mrns(absr, BASE6, ka["fbsk"], ka["ksk"], PA)
-    bl, mx = silenzio.mrns_bitlen_max(dabs, ka["fbsk"], ka["ksk"], PA)
-    Y, mb = silenzio.mrns_digit_combine(digits[-1].contiguous(), dabs, mx, BASE6[-1], W_BITS, GAMMA_SIGNED - 1,
-                                        ka, PA, g["kb"], PB, g["ksk_ab"], g["pab"], g["ksk_ba"], g["pba"])
-    return Y, mb, digits, dabs, mx
+    Y, mb = silenzio.shift2msbs_pm(res_ct, BASE6, W_BITS, GAMMA_SIGNED - 1, g["ka"], PA, g["kb"], PB,
+                                   g["ksk_ab"], g["pab"], g["ksk_ba"], g["pba"])
+    return Y, mb, None, None, None
 
 
 def test_config4_tiny_gpu_vs_oracle(dev):
