@@ -6,7 +6,6 @@ import numpy as np
 import pytest
 import torch
 
-import oracle
 from oracle import noise
 from synth import get_params, key_randomness, lut_ids, lut_tables, lwe_randomness, messages
 
