@@ -105,6 +105,31 @@ class Context:
         """clip(W - G) for G in {-1, 0, 1} (silenzio_weight_update)."""
         return sz.weight_update(W, G, wmin, wmax, self.ka["fbsk"], self.ka["ksk"], self.PA, stream=stream)
 
+    def _spawn(self, fn):
+        """Start fn(stream) in a background host thread on a new stream ordered
+        after the current stream's work; returns a handle for _join."""
+        import concurrent.futures as cf
+        cur = torch.cuda.current_stream(self.dev)
+        st = torch.cuda.Stream(device=self.dev)
+        st.wait_stream(cur)
+        ex = cf.ThreadPoolExecutor(1)
+
+        def run():
+            with torch.cuda.stream(st):
+                return fn(st)
+        return ex, ex.submit(run), st
+
+    def _join(self, job):
+        ex, fut, st = job
+        out = fut.result()
+        ex.shutdown()
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_stream(st)
+        for t in (out if isinstance(out, (tuple, list)) else (out,)):
+            if isinstance(t, torch.Tensor):
+                t.record_stream(cur)
+        return out
+
     def _par(self, *fns):
         """Run independent gadget chains concurrently: each on its own CUDA stream
         (ordered after the current stream's work) in its own host thread (the
@@ -161,6 +186,7 @@ class Context:
         tick("ce grad")
         inter["errs"].append(E)
         newW = [None] * L
+        pending = []
         for l in range(L - 1, -1, -1):
             W = Ws[l]
             c_l, b_l = W.shape[0], W.shape[1]
@@ -181,14 +207,17 @@ class Context:
                 En = self.sign3(Em.reshape(len(ebase), a * b_l, -1), ebase, st)
                 return self.relu_mask(En, pre[l - 1].reshape(a * b_l, -1), cap, st).reshape(a, b_l, -1)
 
+            # the gradient branch of layer l is needed only at the end: it runs
+            # in the background while the error propagates to the layers below
+            pending.append((l, self._spawn(grad_branch)))
             if l > 0:
-                (G, nw), E = self._par(grad_branch, err_branch)
+                E = err_branch(None)
                 inter["errs"].append(E)
-            else:
-                G, nw = grad_branch(None)
-            inter["grads"].insert(0, G)
-            newW[l] = nw
-            tick("backward (gradient | error branches) + update")
+        grads = [None] * L
+        for l, job in pending:
+            grads[l], newW[l] = self._join(job)
+        inter["grads"] = grads
+        tick("backward (gradient | error branches) + update")
         inter["pre"], inter["acts"] = pre, acts
         if times is not None:
             times.pop("_t")
