@@ -735,9 +735,19 @@ __device__ __forceinline__ void cl_mbar_init(uint32_t mbar, uint32_t count) {
 __device__ __forceinline__ void cl_mbar_expect(uint32_t mbar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
 }
+#ifndef SZ_SETB_RELFENCE
+#define SZ_SETB_RELFENCE 1  // one release fence + relaxed arrives (0: a release-arrive per remote barrier)
+#endif
 // release-arrive on a barrier of another CTA of the cluster
 __device__ __forceinline__ void cl_mbar_arrive_remote(uint32_t rmbar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rmbar) : "memory");
+}
+// relaxed arrive: ordering comes from a preceding fence.release.cluster (ptxas
+// emits the full MEMBAR.GPU + ERRBAR sequence once per fence instead of once per
+// release-arrive)
+__device__ __forceinline__ void cl_fence_release() { asm volatile("fence.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void cl_mbar_arrive_remote_relaxed(uint32_t rmbar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(rmbar) : "memory");
 }
 __device__ __forceinline__ void cl_mbar_wait_acq(uint32_t mbar, uint32_t parity) {
   asm volatile(
@@ -792,8 +802,14 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
   auto release_buf = [&]() {  // after a __syncthreads: this CTA is done with its buffer
     if (t == 0) {
       cl_mbar_expect(full, 4 * 1024 * sizeof(double2));
+      if (SZ_SETB_RELFENCE) {
+        cl_fence_release();
 #pragma unroll
-      for (int r = 0; r < kClQ; r++) cl_mbar_arrive_remote(cl_mapa(freeb, r));
+        for (int r = 0; r < kClQ; r++) cl_mbar_arrive_remote_relaxed(cl_mapa(freeb, r));
+      } else {
+#pragma unroll
+        for (int r = 0; r < kClQ; r++) cl_mbar_arrive_remote(cl_mapa(freeb, r));
+      }
     }
   };
   if (SZ_SETB_ASYNCX) {
