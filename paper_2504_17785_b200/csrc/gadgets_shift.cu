@@ -87,10 +87,17 @@ int silenzio_shift2msbs_pm(const uint64_t *residues, const uint32_t *moduli_host
   cudaStream_t sb = nullptr;
   cudaEvent_t ready = nullptr;
   SZ_CUDA_OK(cudaStreamCreateWithFlags(&sb, cudaStreamNonBlocking));
-  SZ_CUDA_OK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  // the second stream and its event are released on every return path below
+  auto finish = [&](int code) {
+    if (sb) cudaStreamSynchronize(sb);
+    if (ready) cudaEventDestroy(ready);
+    cudaStreamDestroy(sb);
+    return code;
+  };
+  if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess) return finish(SILENZIO_ERR_CUDA);
   // stream B starts after everything already queued on the caller's stream
-  SZ_CUDA_OK(cudaEventRecord(ready, sa));
-  SZ_CUDA_OK(cudaStreamWaitEvent(sb, ready, 0));
+  if (cudaEventRecord(ready, sa) != cudaSuccess || cudaStreamWaitEvent(sb, ready, 0) != cudaSuccess)
+    return finish(SILENZIO_ERR_CUDA);
   int rc_b = SILENZIO_OK;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -103,17 +110,14 @@ int silenzio_shift2msbs_pm(const uint64_t *residues, const uint32_t *moduli_host
   int rc = silenzio_rns2mrns(residues, moduli_host, k, count, digits, fbsk_a, ksk_a, pa, ws_a, g, sa);
   chain_b.join();
   if (!rc) rc = rc_b;
+  if (!rc && (cudaEventRecord(ready, sb) != cudaSuccess || cudaStreamWaitEvent(sa, ready, 0) != cudaSuccess))
+    rc = SILENZIO_ERR_CUDA;
   if (!rc) {
-    SZ_CUDA_OK(cudaEventRecord(ready, sb));
-    SZ_CUDA_OK(cudaStreamWaitEvent(sa, ready, 0));
     rc = silenzio_mrns_digit_combine(digits + (size_t)(k - 1) * count * cw, dabs, mx, k, count, moduli_host[k - 1],
                                      w, gamma, out, maxbit_out, fbsk_a, ksk_a, pa, fbsk_b, pb, ksk_ab, pab, ksk_ba,
                                      pba, ws_c, ws_c_bytes, sa);
   }
-  cudaStreamSynchronize(sb);
-  cudaEventDestroy(ready);
-  cudaStreamDestroy(sb);
-  return rc;
+  return finish(rc);
 }
 
 }  // extern "C"
