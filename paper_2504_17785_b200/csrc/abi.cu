@@ -244,11 +244,11 @@ int silenzio_pbs_batch_host(const uint64_t *in_h, const uint32_t *ids_h, const u
   const size_t in_b = round_up(chunk * big * 8, 256), id_b = round_up(chunk * 4, 256);
   const size_t ws_b = silenzio_pbs_workspace_bytes(P, chunk);
   const size_t per = in_b * 2 + id_b + ws_b;
-  cudaStream_t s[2];
-  cudaEvent_t done[2];
-  for (int i = 0; i < 2; i++) {
-    if (cudaStreamCreateWithFlags(&s[i], cudaStreamNonBlocking) != cudaSuccess) return SILENZIO_ERR_CUDA;
-    if (cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  cudaStream_t s[2] = {nullptr, nullptr};
+  if (cudaStreamCreateWithFlags(&s[0], cudaStreamNonBlocking) != cudaSuccess) return SILENZIO_ERR_CUDA;
+  if (cudaStreamCreateWithFlags(&s[1], cudaStreamNonBlocking) != cudaSuccess) {
+    cudaStreamDestroy(s[0]);
+    return SILENZIO_ERR_CUDA;
   }
   int rc = SILENZIO_OK;
   // Two stages alternate; each chunk: H2D in, PBS, D2H out on its stage's
@@ -276,7 +276,6 @@ int silenzio_pbs_batch_host(const uint64_t *in_h, const uint32_t *ids_h, const u
   }
   for (int i = 0; i < 2; i++) {
     if (cudaStreamSynchronize(s[i]) != cudaSuccess) rc = SILENZIO_ERR_CUDA;
-    cudaEventDestroy(done[i]);
     cudaStreamDestroy(s[i]);
   }
   return rc;
