@@ -189,6 +189,9 @@ __host__ __device__ constexpr size_t brl_smem_bytes(int n) {
 #ifndef SZ_L2PF
 #define SZ_L2PF 1  // bulk L2 prefetch of the next MAC round's Fourier-BSK rows (set C: +1.7 %)
 #endif
+#ifndef SZ_L2PF_AHEAD
+#define SZ_L2PF_AHEAD 1  // MAC rounds ahead the set-C prefetch runs
+#endif
 #ifndef SZ_L2PF_B
 #define SZ_L2PF_B 0  // the same on the set-B cluster kernel: measured 3-6 % slower, off
 #endif
@@ -242,7 +245,13 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
           l2_prefetch_bulk(A.fbsk + (((size_t)i * 2 + o) * rows + row) * P * kML + (size_t)p * kML,
                            kML * sizeof(double2));
     };
-    prefetch_round(0, 0, P - 1);
+    // MAC round k of CMux i (k = o P + P - 1 - p, 2P rounds) -> prefetch k + SZ_L2PF_AHEAD
+    auto prefetch_ahead = [&](int i, int k) {
+      i += k / (2 * P);
+      k %= 2 * P;
+      prefetch_round(i, k / P, P - 1 - k % P);
+    };
+    for (int k = 0; k < SZ_L2PF_AHEAD; k++) prefetch_ahead(0, k);
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
       // -------- forward: every (component r, level lvl) digit polynomial
@@ -296,9 +305,7 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
         u64 *acco = acc + o * kNL;
 #pragma unroll 1
         for (int p = P - 1; p >= 0; p--) {
-          if (p > 0) prefetch_round(i, o, p - 1);
-          else if (o == 0) prefetch_round(i, 1, P - 1);
-          else prefetch_round(i + 1, 0, P - 1);
+          prefetch_ahead(i, o * P + (P - 1 - p) + SZ_L2PF_AHEAD);
           double2 y[16];
 #pragma unroll
           for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
