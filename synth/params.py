@@ -89,6 +89,12 @@ PARAMS = {
     "B_SMALLN": Params("B_SMALLN", n=6, k=1, N=32768, pbs_base_log=15, pbs_level=2,
                        ks_base_log=4, ks_level=5, lwe_sigma_log2=-23.0,
                        glwe_sigma_log2=-51.0, p=8),
+    # Set-B-shaped gadget (2^15 x 2, KS 2^4 x 5, 8-bit + padding) at N = 2048 and
+    # small n: box = N/2^p = 8 positions, enough for the CPU oracle to pin the
+    # 8-bit *compositions* (the N-independent table/packing logic) in seconds.
+    "B_TINYN": Params("B_TINYN", n=8, k=1, N=2048, pbs_base_log=15, pbs_level=2,
+                      ks_base_log=4, ks_level=5, lwe_sigma_log2=-23.0,
+                      glwe_sigma_log2=-51.0, p=8),
     "EXACT32768": Params("EXACT32768", n=3, k=1, N=32768, pbs_base_log=16,
                          pbs_level=4, ks_base_log=8, ks_level=8,
                          lwe_sigma_log2=NOISELESS, glwe_sigma_log2=NOISELESS,
