@@ -10,8 +10,11 @@
  *
  * Everything is exact integer arithmetic mod 2^64 (uint64_t wraps). Polynomial
  * products are schoolbook negacyclic (N^2 multiply-adds, sign flip on wrap):
- * no FFT, no blocking, no reordering. OpenMP only splits independent
- * ciphertexts (or independent key rows) across threads.
+ * no FFT, no blocking, no reordering of the arithmetic. OpenMP splits
+ * independent ciphertexts (or key rows) across threads; at N >= 8192 a batch
+ * smaller than the thread count instead splits the N^2 terms of each external
+ * product into private partial sums added afterwards (exact: integer addition mod 2^64 is
+ * associative and commutative, so the result is bit-identical).
  *
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may load
  * this library. It shares no code with paper_2504_17785_b200/.
@@ -37,17 +40,25 @@ int oracle_num_threads(void) {
 /* out += a * b  in Z_{2^64}[X]/(X^N + 1), schoolbook.
  * Term a_i b_j lands on X^{i+j}; if i+j >= N it wraps to X^{i+j-N} with a
  * minus sign because X^N = -1.  (SURVEY.md §8(c) C6 "schoolbook negacyclic
- * mod 2^64: N^2 u64 MACs with sign flip on wrap".) */
+ * mod 2^64: N^2 u64 MACs with sign flip on wrap".)
+ * _part adds only the terms with i in [i0, i1), so that the N^2 terms of one
+ * product can be split across threads (the sum mod 2^64 does not depend on
+ * the order in which the terms are added). */
 #if defined(__x86_64__) && defined(__GNUC__) && !defined(__clang__)
 __attribute__((target_clones("arch=x86-64-v4", "arch=x86-64-v3", "default")))
 #endif
-void oracle_negacyclic_mac(u64 *out, const u64 *a, const u64 *b, int N) {
-  for (int i = 0; i < N; i++) {
+void oracle_negacyclic_mac_part(u64 *out, const u64 *a, const u64 *b, int N, int i0, int i1) {
+  for (int i = i0; i < i1; i++) {
     const u64 ai = a[i];
     if (ai == 0) continue; /* exact: a zero term adds nothing */
     for (int j = 0; j < N - i; j++) out[i + j] += ai * b[j];
     for (int j = N - i; j < N; j++) out[i + j - N] -= ai * b[j];
   }
+}
+
+/* The full product: the terms a_i b_j for every i (the sum above over i in [0, N)). */
+void oracle_negacyclic_mac(u64 *out, const u64 *a, const u64 *b, int N) {
+  oracle_negacyclic_mac_part(out, a, b, N, 0, N);
 }
 
 /* out = X^e * in, e in [0, 2N) (negacyclic rotation; X^N = -1). */
@@ -207,6 +218,14 @@ void oracle_blind_rotate(const u64 *lwe, const u64 *testpoly, const u64 *bsk, in
   u64 *digit_poly = (u64 *)malloc(sizeof(u64) * rows * N);
   u64 *prod = (u64 *)malloc(sizeof(u64) * K1 * N);
   i64 d[64];
+  /* a large ring (N >= 8192) outside any parallel region (a few ciphertexts):
+   * split each external product across the threads; otherwise stay serial */
+  enum { kSplit = 4 };
+  const int ntask = rows * K1 * kSplit;
+  u64 *part = NULL;
+#ifdef _OPENMP
+  if (N >= 8192 && !omp_in_parallel() && omp_get_max_threads() > 1) part = (u64 *)malloc(sizeof(u64) * ntask * N);
+#endif
 
   /* ACC init: X^{-b~} * v = X^{2N - b~} * v */
   const u64 bt = oracle_modswitch(lwe[n], log2_2N);
@@ -229,16 +248,37 @@ void oracle_blind_rotate(const u64 *lwe, const u64 *testpoly, const u64 *bsk, in
     /* external product with the GGSW BSK_i */
     memset(prod, 0, sizeof(u64) * K1 * N);
     const u64 *G = bsk + (size_t)i * rows * K1 * N;
-    for (int row = 0; row < rows; row++)
-      for (int o = 0; o < K1; o++)
-        oracle_negacyclic_mac(prod + (size_t)o * N, digit_poly + (size_t)row * N,
-                              G + ((size_t)row * K1 + o) * N, N);
+    if (!part) {
+      for (int row = 0; row < rows; row++)
+        for (int o = 0; o < K1; o++)
+          oracle_negacyclic_mac(prod + (size_t)o * N, digit_poly + (size_t)row * N,
+                                G + ((size_t)row * K1 + o) * N, N);
+    } else {
+      /* the same terms, split over (row, o, i-range) tasks into private sums
+       * (one blind rotation alone, e.g. a single set-B PBS, uses every core) */
+#ifdef _OPENMP
+#pragma omp parallel for schedule(dynamic)
+#endif
+      for (int t = 0; t < ntask; t++) {
+        const int row = t / (K1 * kSplit), o = (t / kSplit) % K1, s = t % kSplit;
+        u64 *dst = part + (size_t)t * N;
+        memset(dst, 0, sizeof(u64) * N);
+        oracle_negacyclic_mac_part(dst, digit_poly + (size_t)row * N, G + ((size_t)row * K1 + o) * N, N,
+                                   s * N / kSplit, (s + 1) * N / kSplit);
+      }
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+      for (int c = 0; c < N; c++)
+        for (int t = 0; t < ntask; t++) prod[(size_t)((t / kSplit) % K1) * N + c] += part[(size_t)t * N + c];
+    }
     for (size_t c = 0; c < (size_t)K1 * N; c++) acc[c] += prod[c];
   }
   free(rot);
   free(diff);
   free(digit_poly);
   free(prod);
+  free(part);
 }
 
 /* Sample extraction of coefficient 0:
@@ -258,7 +298,7 @@ void oracle_pbs(const u64 *lwe_in, const uint32_t *lut_ids, const u64 *luts, int
                 const u64 *bsk, const u64 *ksk, u64 *lwe_out, long count, int n, int k,
                 int N, int pbs_base_log, int pbs_level, int ks_base_log, int ks_level) {
   const int big = k * N;
-#pragma omp parallel for schedule(dynamic)
+#pragma omp parallel for schedule(dynamic) if (count >= oracle_num_threads() || N < 8192)
   for (long c = 0; c < count; c++) {
     u64 *small = (u64 *)malloc(sizeof(u64) * (n + 1));
     u64 *acc = (u64 *)malloc(sizeof(u64) * (k + 1) * N);
@@ -280,7 +320,7 @@ void oracle_br_se(const u64 *lwe_small, const uint32_t *lut_ids, const u64 *luts
                   int num_luts, const u64 *bsk, u64 *lwe_out, long count, int n, int k,
                   int N, int pbs_base_log, int pbs_level) {
   const int big = k * N;
-#pragma omp parallel for schedule(dynamic)
+#pragma omp parallel for schedule(dynamic) if (count >= oracle_num_threads() || N < 8192)
   for (long c = 0; c < count; c++) {
     u64 *acc = (u64 *)malloc(sizeof(u64) * (k + 1) * N);
     uint32_t id = lut_ids ? lut_ids[c] : 0;
