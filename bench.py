@@ -28,7 +28,33 @@ sys.path.insert(0, ROOT)
 
 METRIC = "PBS/sec (4-bit, N=2048) on 1 B200; % of FP64/HBM PBS roofline"
 UNIT = "PBS/s"
-FP64_PEAK_TFLOPS = 33.6  # measured DFMA burst peak, tools/microbench (profiles/fp64_peak.txt)
+PEAK_FILE = os.path.join(ROOT, "profiles", "r02_fp64_peak.json")      # tools/fp64_peak.py (with its clock log)
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_br_traffic.json")   # tools/ncu_traffic.py
+
+
+def fp64_peak() -> dict:
+    """The FP64 roofline denominator: the measured DFMA burst peak of
+    tools/microbench/fp64_peak.cu (best of 10 launches per shape, six shapes;
+    sustained 4 s run and the nvidia-smi clock log in the same file)."""
+    with open(PEAK_FILE) as f:
+        pk = json.load(f)
+    return {"tflops": float(pk["burst_tflops"]), "sustained_tflops": float(pk["sustained_tflops"]),
+            "clock_derived_tflops": float(pk["clock_derived_tflops"]),
+            "sm_mhz": pk.get("sm_mhz_median_under_load"), "source": os.path.relpath(PEAK_FILE, ROOT)}
+
+
+def br_traffic(batch: int, config: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the bench's own BR launch
+    from the committed ncu capture of the same command (None if it was captured
+    for another batch / config)."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return None, None
+    if t.get("batch") != batch or t.get("config") != config:
+        return None, None
+    return float(t["dram_read_bytes"]) + float(t["dram_write_bytes"]), t
 
 
 def pbs_flops(P) -> float:
@@ -292,30 +318,37 @@ def main():
         return
 
     flops = pbs_flops(P)
+    pk = fp64_peak()
+    fp64_tf = pk["tflops"]
+    traffic, traffic_rec = br_traffic(B, args.config)
     ks_ops = 2.0 * P.big_dim * P.ks_level * (P.n + 1) * 8  # 8 byte-plane int8 GEMM MACs per ciphertext
     launches = int(args.steps * silenzio.pbs_launch_count(P, B))
     br_avg_s = float(np.mean(br_ms)) / 1e3
     achieved = flops * B / br_avg_s / 1e12
-    roofline = {"bound": "alu", "pipe": "fp64", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                # dram__bytes_read.sum + dram__bytes_write.sum of the bench's own BR launch, measured by ncu
-                # for the default 131072-ciphertext batch (null for other batch sizes: not measured)
-                "traffic": 1.868252e12 if (B == 131072 and args.config == 1) else None,
-                "traffic_source": "profiles/r01_ncu_br_bench_dram.txt: dram__bytes_read.sum + dram__bytes_write.sum "
-                                  "of the bench's 131072-ciphertext launch (the drifting persistent grid re-reads the "
-                                  "146 MB Fourier BSK; HBM stays at ~10 % of its bandwidth, see DESIGN.md §6)",
+    roofline = {"bound": "alu", "pipe": "fp64", "achieved": achieved, "peak": fp64_tf,
+                "unit": "TFLOP/s", "frac": achieved / fp64_tf,
+                # dram__bytes_read.sum + dram__bytes_write.sum of the bench's own BR launch (ncu, committed capture
+                # of the same command; null when the committed capture is for another batch or config)
+                "traffic": traffic,
+                "traffic_source": (f"{os.path.relpath(TRAFFIC_FILE, ROOT)}: {traffic_rec.get('command')}"
+                                   if traffic_rec else "not captured for this batch/config"),
+                "algorithmic_bytes": float(silenzio.fourier_bsk_bytes(P) + B * (P.n + 1) * 8
+                                           + B * (P.big_dim + 1) * 8 + 8 * P.N * 8),
                 "kernel": "blind_rotate_warp_kernel<3>", "algorithmic_flops_per_pbs": flops,
                 "kernel_ms": float(np.mean(br_ms)), "keyswitch_ms": float(np.mean(ks_ms)),
-                "peak_source": "measured DFMA burst (tools/microbench/mb.cu, profiles/r01_microbench_b200.txt)",
+                "peak_source": (f"{pk['source']}: measured DFMA burst (best of 10 launches, six shapes, "
+                                f"{pk['sm_mhz']} MHz); sustained {pk['sustained_tflops']:.2f}, "
+                                f"clock-derived 148x64x2xf_max = {pk['clock_derived_tflops']:.2f}"),
+                "frac_vs_clock_derived_peak": achieved / pk["clock_derived_tflops"],
                 "keyswitch": {"kernel": "keyswitch_tc_kernel<5> (tcgen05 kind::i8)",
                               "int8_tensor_tops": ks_ops * B / (float(np.mean(ks_ms)) / 1e3) / 1e12,
                               "peak_int8_tops_nominal": 4500.0,
                               "ops_per_ct": ks_ops},
-                "pbs_roofline_pbs_per_s": FP64_PEAK_TFLOPS * 1e12 / flops,
+                "pbs_roofline_pbs_per_s": fp64_tf * 1e12 / flops,
                 # the stricter P = 1 denominator beside it (an approximate single-limb
                 # FFT would need only these flops, but cannot meet the 2^-32 parity bound, DESIGN R20)
-                "frac_vs_p1_flops": (pbs_flops(P.with_(fft_limbs=1)) * B / br_avg_s / 1e12) / FP64_PEAK_TFLOPS,
-                "frac_of_pbs_roofline_whole_step": value / world / (FP64_PEAK_TFLOPS * 1e12 / flops)}
+                "frac_vs_p1_flops": (pbs_flops(P.with_(fft_limbs=1)) * B / br_avg_s / 1e12) / fp64_tf,
+                "frac_of_pbs_roofline_whole_step": value / world / (fp64_tf * 1e12 / flops)}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64", "data": "synthetic",

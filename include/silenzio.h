@@ -311,6 +311,27 @@ int silenzio_ksk_generate(const uint64_t *in_key, const uint64_t *lwe_key, const
                           const int64_t *noise, uint64_t *ksk, uint32_t in_dim, uint32_t n,
                           uint32_t base_log, uint32_t level, void *stream);
 
+/* ------------------------------------------ sampled-PBS trace (test / debug)
+ * The gadget drivers evaluate their PBS internally; an oracle replay of a
+ * sample of them ("Replay 1 024 sampled PBS" of configs 3 and
+ * 4) needs their inputs. While a trace of `kind` is active, every `stride`-th
+ * PBS element (global element counter across calls, offset `phase` < stride)
+ * evaluated by that kind of call site is copied, stream-ordered, into
+ * `records` (DEVICE, [max_records][in_words + out_words + lut_words + 2] u64):
+ *   [input LWE][output LWE][test polynomial][global element index, lut id].
+ * kind 0: set-A PBS of the gadget drivers (in/out: big-key LWE, k*N+1 words;
+ *         lut: N words). kind 1: the set-B blind rotation + sample extraction
+ *         of the 8-bit stage (in: set-B small-key LWE, n+1 words; out: set-B
+ *         big-key LWE, k*N+1 words; lut: N words).
+ * Records whose sizes do not match the call site are skipped (counted only).
+ * Process-wide state (one trace per kind, mutex-guarded); off by default,
+ * and the drivers' results do not depend on it. end() stops the trace and
+ * returns the number of records written (or a negative status), and the
+ * number of elements seen through `elements_seen` (may be NULL). */
+int silenzio_pbs_trace_begin(int kind, uint64_t *records, size_t max_records, uint64_t stride, uint64_t phase,
+                             size_t in_words, size_t out_words, size_t lut_words);
+long silenzio_pbs_trace_end(int kind, uint64_t *elements_seen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,10 @@ size_t silenzio_pbs_workspace_bytes(const silenzio_params *, size_t);
 }
 
 namespace sz {
+// trace.cu: sampled-PBS recording for oracle replays (no-op unless a trace is active)
+bool trace_active(int kind);
+void trace_pbs(int kind, const u64 *in, size_t in_words, const u64 *out, size_t out_words, const u64 *luts,
+               size_t lut_words, const u32 *ids_host, size_t count, cudaStream_t st);
 int launch_lwe_axpy3(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc, u64 cst,
                      size_t count, int dim, cudaStream_t st);
 int launch_lwe_axpy_bcast(u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc, size_t count,
@@ -109,6 +113,9 @@ inline int lookup(Dev &D, const u64 *in, u64 *out, size_t count, const std::vect
     int rc = silenzio_pbs_batch(in + c0 * D.big, idp, D.luts, num_luts, D.fbsk, D.ksk, out + c0 * D.big, cnt, D.P,
                                 D.pbs_ws, D.st);
     if (rc) return rc;
+    if (trace_active(0))
+      trace_pbs(0, in + c0 * D.big, D.big, out + c0 * D.big, D.big, D.luts, D.P->poly_size,
+                ids.empty() ? nullptr : ids.data() + c0, cnt, D.st);
   }
   return SILENZIO_OK;
 }

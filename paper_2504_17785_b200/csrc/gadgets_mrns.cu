@@ -372,6 +372,9 @@ int pbs_b(DevB &B, const u64 *in, u64 *out, size_t count, u32 num_luts, const st
     if (rc) return rc;
     if ((rc = silenzio_blind_rotate_batch(B.small, idp, B.luts, num_luts, B.fbsk, B.big, cnt, B.pb, B.brws, B.st)))
       return rc;
+    if (trace_active(1))
+      trace_pbs(1, B.small, (size_t)B.pb->lwe_dim + 1, B.big, (size_t)B.pb->glwe_dim * B.pb->poly_size + 1, B.luts,
+                B.pb->poly_size, ids.empty() ? nullptr : ids.data() + c0, cnt, B.st);
     if ((rc = silenzio_keyswitch_batch(B.big, B.ksk_ba, out + c0 * ca, cnt, B.pba, nullptr, B.st))) return rc;
   }
   return SILENZIO_OK;

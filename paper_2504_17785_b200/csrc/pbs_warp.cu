@@ -52,72 +52,7 @@ struct C32 {
       0.9807852804032304};
 };
 
-// multiply by W_32^E = e^{+2 pi i E / 32} (conjugate when INV)
-template <int E, bool INV>
-__device__ __forceinline__ double2 mulw32(double2 a) {
-  constexpr int e = INV ? ((32 - (E & 31)) & 31) : (E & 31);
-  if constexpr (e == 0) {
-    return a;
-  } else if constexpr (e == 8) {
-    return make_double2(-a.y, a.x);
-  } else if constexpr (e == 16) {
-    return make_double2(-a.x, -a.y);
-  } else if constexpr (e == 24) {
-    return make_double2(a.y, -a.x);
-  } else {
-    constexpr double c = C32::c[e];
-    constexpr double s = C32::c[(e + 24) & 31];  // sin(2 pi e/32) = cos(2 pi (e-8)/32)
-    return make_double2(fma(a.x, c, -a.y * s), fma(a.x, s, a.y * c));
-  }
-}
-
-template <bool INV>
-__device__ __forceinline__ double2 mulw32v(double2 d, int e) {
-  switch (e & 31) {
-#define SZ_W(k) \
-  case k: return mulw32<k, INV>(d);
-    SZ_W(0) SZ_W(1) SZ_W(2) SZ_W(3) SZ_W(4) SZ_W(5) SZ_W(6) SZ_W(7)
-    SZ_W(8) SZ_W(9) SZ_W(10) SZ_W(11) SZ_W(12) SZ_W(13) SZ_W(14) SZ_W(15)
-#undef SZ_W
-    default: return d;
-  }
-}
-
-// Variant switches. All 64 combinations were built (tools/build_warp_variants.sh)
-// and timed on a B200 (profiles/r01_warp_variants.txt): the spread is 31-40.5 k
-// PBS/s from register allocation and scheduling alone; the defaults are the fastest.
-#ifndef SZ_DFT_DIT
-#define SZ_DFT_DIT 1  // DIT with 6-op FMA butterflies (9 % fewer FP64 ops than DIF)
-#endif
-#ifndef SZ_TW_SMEM
-#define SZ_TW_SMEM 0  // four-step twiddles staged in shared memory (one swizzled table)
-#endif
-#ifndef SZ_ACC_FAST
-#define SZ_ACC_FAST 2  // limb recombination without per-limb offset correction (2: branch-free, +0.7 %; 1: per-limb branches, -14 %)
-#endif
-#ifndef SZ_INV_TW_POST
-#define SZ_INV_TW_POST 1  // inverse untwiddle after the transposition
-#endif
-#ifndef SZ_MAC_X32
-#define SZ_MAC_X32 1  // 32-column TMEM loads of the digit spectra in the MAC
-#endif
-
-// Radix-2 decimation-in-frequency stages (natural in, bit-reversed out), half size H = 16..1
-template <bool INV, int H>
-__device__ __forceinline__ void dif32_stage(double2 (&x)[32]) {
-  if constexpr (H >= 1) {
-#pragma unroll
-    for (int b = 0; b < 32; b += 2 * H)
-#pragma unroll
-      for (int j = 0; j < H; j++) {
-        const double2 a = x[b + j], c = x[b + j + H];
-        x[b + j] = cadd(a, c);
-        x[b + j + H] = mulw32v<INV>(csub(a, c), j * (16 / H));  // W_{2H}^j = W_32^{j 32/(2H)}
-      }
-    dif32_stage<INV, H / 2>(x);
-  }
-}
-
+// Radix-2 decimation-in-time butterflies.
 // tan(2 pi r / 32), r = 0..4 (correctly rounded doubles)
 struct T32 {
   static constexpr double t[5] = {0.0, 0.198912367379658, 0.41421356237309503, 0.6681786379192989, 1.0};
@@ -127,9 +62,8 @@ struct T32 {
 // when INV), 6 FP64 instructions when nontrivial: with W^e = i^q e^{i theta},
 //   e^{i theta} b = cos (b.x - tan b.y, b.y + tan b.x) = sin (cot b.x - b.y, cot b.y + b.x)
 // and the cos / sin scale folds into the four output FMAs.
-// R: pending-scale ratio s_b / s_a (1 unless inputs carry factored-out twist scales)
 template <int E, bool INV>
-__device__ __forceinline__ void bfly(double2 &a, double2 &b, double R = 1.0) {
+__device__ __forceinline__ void bfly(double2 &a, double2 &b) {
   constexpr int e = INV ? ((32 - (E & 31)) & 31) : (E & 31);
   constexpr int q = e >> 3, r = e & 7;
   if constexpr (r == 0) {
@@ -138,16 +72,9 @@ __device__ __forceinline__ void bfly(double2 &a, double2 &b, double R = 1.0) {
     else if constexpr (q == 1) t = make_double2(-b.y, b.x);
     else if constexpr (q == 2) t = make_double2(-b.x, -b.y);
     else t = make_double2(b.y, -b.x);
-    if (R == 1.0) {
-      const double2 na = cadd(a, t), nb = csub(a, t);
-      a = na;
-      b = nb;
-    } else {
-      const double2 na = make_double2(fma(R, t.x, a.x), fma(R, t.y, a.y));
-      const double2 nb = make_double2(fma(-R, t.x, a.x), fma(-R, t.y, a.y));
-      a = na;
-      b = nb;
-    }
+    const double2 na = cadd(a, t), nb = csub(a, t);
+    a = na;
+    b = nb;
   } else {
     double u, v;
     if constexpr (r <= 4) {
@@ -159,7 +86,7 @@ __device__ __forceinline__ void bfly(double2 &a, double2 &b, double R = 1.0) {
       u = fma(ct, b.x, -b.y);
       v = fma(ct, b.y, b.x);
     }
-    const double f = ((r <= 4) ? C32::c[r] : C32::c[8 - r]) * R;  // folded at compile time
+    constexpr double f = (r <= 4) ? C32::c[r] : C32::c[8 - r];
     double U, V;  // (u + i v) * i^q
     if constexpr (q == 0) { U = u; V = v; }
     else if constexpr (q == 1) { U = -v; V = u; }
@@ -198,9 +125,6 @@ __host__ __device__ constexpr int bitrev5(int r) {
   return ((r & 1) << 4) | ((r & 2) << 2) | (r & 4) | ((r & 8) >> 2) | ((r & 16) >> 4);
 }
 
-#ifndef SZ_TAN_TWIST
-#define SZ_TAN_TWIST 2  // sweep 3 (profiles/r01_warp_variants3.txt): 2 with the XOR swizzle is fastest (47.0 k BR-only); with padding it lost to I-cache misses. bit 0: forward, bit 1: inverse (fused with the rounding); negacyclic w^{32m} twist as 2 FMAs (tangent form), scale folded into the DFT / rounding
-#endif
 // cos(pi k / 64), tan(pi k / 64), k = 0..16 (correctly rounded doubles)
 struct C64 {
   static constexpr double c[17] = {
@@ -214,71 +138,28 @@ struct C64 {
       0.5345111359507917, 0.5993769336819238, 0.6681786379192989, 0.7416505462720354, 0.8206787908286604,
       0.9063471690191471, 1.0};
 };
-// w^{32m} = e^{i th}, th = pi m / 64 < pi/2, written as  s_m * (unscaled factor):
-//   m <= 16: cos th (1 + i tan th)      m > 16: sin th (cot th + i)
-// s_m = twist_scale(m); the unscaled product costs 2 FMAs instead of a 4-op complex multiply.
+// conj(w^{32m}) = e^{-i th}, th = pi m / 64 < pi/2, written as s_m * (unscaled factor):
+//   m <= 16: cos th (1 - i tan th)      m > 16: sin th (cot th - i)
+// the unscaled product costs 2 FMAs; s_m folds into the rounding FMA.
 __host__ __device__ constexpr double twist_scale(int m) { return m <= 16 ? C64::c[m] : C64::c[32 - m]; }
-template <int M, bool INV>
-__device__ __forceinline__ double2 twist_unscaled(double2 a) {
+template <int M>
+__device__ __forceinline__ double2 untwist_unscaled(double2 a) {
   if constexpr (M == 0) {
     return a;
   } else if constexpr (M <= 16) {
     constexpr double t = C64::t[M];
-    return INV ? make_double2(fma(t, a.y, a.x), fma(-t, a.x, a.y)) : make_double2(fma(-t, a.y, a.x), fma(t, a.x, a.y));
+    return make_double2(fma(t, a.y, a.x), fma(-t, a.x, a.y));
   } else {
     constexpr double ct = C64::t[32 - M];
-    return INV ? make_double2(fma(ct, a.x, a.y), fma(ct, a.y, -a.x)) : make_double2(fma(ct, a.x, -a.y), fma(ct, a.y, a.x));
+    return make_double2(fma(ct, a.x, a.y), fma(ct, a.y, -a.x));
   }
-}
-template <bool INV, int M>
-__device__ __forceinline__ void twist_all_unscaled(double2 (&x)[32]) {
-  if constexpr (M < 32) {
-    x[M] = twist_unscaled<M, INV>(x[M]);
-    twist_all_unscaled<INV, M + 1>(x);
-  }
-}
-
-// DIT stages on inputs that carry pending scales (the factored-out twist
-// scales): before stage H the value at bit-reversed position e carries
-// s(bitrev5(e & ~(H-1))). Butterfly (B+J, B+J+H) computes a + (s_b/s_a) W b,
-// a - (s_b/s_a) W b and both keep s_a; the ratio folds into the butterfly's
-// FMA constants (no extra instructions), and after the last stage every output
-// carries s(bitrev5(0)) = 1.
-template <bool INV, int H, int B, int J>
-__device__ __forceinline__ void dits_bf(double2 (&y)[32]) {
-  if constexpr (B < 32) {
-    if constexpr (J < H) {
-      constexpr double R = twist_scale(bitrev5(B + H)) / twist_scale(bitrev5(B));
-      bfly<J * (16 / H), INV>(y[B + J], y[B + J + H], R);
-      dits_bf<INV, H, B, J + 1>(y);
-    } else {
-      dits_bf<INV, H, B + 2 * H, 0>(y);
-    }
-  }
-}
-template <bool INV, int H>
-__device__ __forceinline__ void dits_stage(double2 (&y)[32]) {
-  if constexpr (H <= 16) {
-    dits_bf<INV, H, 0, 0>(y);
-    dits_stage<INV, 2 * H>(y);
-  }
-}
-// X[k] = sum_m s_m x[m] e^{+-2 pi i m k / 32} for inputs x[m] = (true value) / s_m
-template <bool INV>
-__device__ __forceinline__ void dft32_scaled(double2 (&x)[32]) {
-  double2 y[32];
-#pragma unroll
-  for (int r = 0; r < 32; r++) y[r] = x[bitrev5(r)];
-  dits_stage<INV, 1>(y);
-#pragma unroll
-  for (int r = 0; r < 32; r++) x[r] = y[r];
 }
 
 // inverse untwist of output m fused with the exact rounding of the limb:
 // bits(s_m * u + 1.5 * 2^52) = round(x conj(w^{32m})) + bits(1.5 * 2^52), |.| < 2^51
 template <int M>
 __device__ __forceinline__ void untwist_round_t(double2 y, u64 &bx, u64 &by) {
-  const double2 u = twist_unscaled<M, true>(y);
+  const double2 u = untwist_unscaled<M>(y);
   constexpr double s = twist_scale(M);
   bx = (u64)__double_as_longlong(fma(u.x, s, 6755399441055744.0));
   by = (u64)__double_as_longlong(fma(u.y, s, 6755399441055744.0));
@@ -297,48 +178,32 @@ __device__ __forceinline__ void untwist_round(double2 y, int m, u64 &bx, u64 &by
 
 // 32-point DFT on registers, exponent sign + (conjugate when INV), natural-order
 // input and output: X[k] = sum_n x[n] e^{+-2 pi i n k / 32}; the bit reversal
-// of either radix-2 form is a register renaming.
+// of the radix-2 DIT form is a register renaming.
 template <bool INV>
 __device__ __forceinline__ void dft32(double2 (&x)[32]) {
   double2 y[32];
-#if SZ_DFT_DIT
 #pragma unroll
   for (int r = 0; r < 32; r++) y[r] = x[bitrev5(r)];
   dit32_stage<INV, 1>(y);
 #pragma unroll
   for (int r = 0; r < 32; r++) x[r] = y[r];
-#else
-#pragma unroll
-  for (int r = 0; r < 32; r++) y[r] = x[r];
-  dif32_stage<INV, 16>(y);
-#pragma unroll
-  for (int r = 0; r < 32; r++) x[bitrev5(r)] = y[r];
-#endif
 }
 
 // Tables (host-built in long double, rounded once), w = e^{i pi / 2048}:
-//   T(l, k1)     = w^{l (1 + 4 k1)}  (negacyclic twist w^l folded with the
-//                  four-step twiddle e^{2 pi i l k1 / M}), stored as
-//   tw [k1 * 32 + l], twT[l * 32 + k1] (coalesced for lane = l / lane = k1) and
-//   tws[sw(l, k1)]  (swizzled, for the shared-memory copy: conflict free both ways)
-//   c_twist32[m]  = w^{32 m} = e^{i pi m / 64}
+//   T(l, k1)   = w^{l (1 + 4 k1)}  (negacyclic twist w^l folded with the
+//                four-step twiddle e^{2 pi i l k1 / M}), stored as tw[k1 * 32 + l]
+//                (coalesced for lane = l)
+//   c_twist32[m] = w^{32 m} = e^{i pi m / 64}
 struct Tables32 {
   double2 tw[32 * 32];
-  double2 twT[32 * 32];
-  double2 tws[32 * 33];
 };
 __device__ Tables32 g_t32;
 __constant__ double2 c_twist32[32];
 
 // swizzled index of element (row, col) of a 32 x 32 block of 16-byte values:
 // any 8 consecutive rows (fixed col) or cols (fixed row) hit 8 distinct 16-byte bank groups
-#ifndef SZ_PAD
-#define SZ_PAD 0  // 1: padded rows (stride 33) instead of the XOR swizzle (sweep 3: XOR swizzle + SZ_TAN_TWIST 2 fastest)
-#endif
-__host__ __device__ constexpr int sw(int row, int col) {
-  return SZ_PAD ? row * 33 + col : row * 32 + (col ^ (row & 7));
-}
-constexpr int kXbuf = SZ_PAD ? 32 * 33 : 1024;  // double2 per transposition buffer
+__host__ __device__ constexpr int sw(int row, int col) { return row * 32 + (col ^ (row & 7)); }
+constexpr int kXbuf = 1024;  // double2 per transposition buffer
 
 static std::once_flag g_once[64];
 static int g_status[64];
@@ -350,10 +215,7 @@ static int init_tables(int dev) {
   for (int k1 = 0; k1 < 32; k1++)
     for (int l = 0; l < 32; l++) {
       const long double ang = PI * (long double)(l * (1 + 4 * k1)) / 2048.0L;
-      const double2 v = make_double2((double)cosl(ang), (double)sinl(ang));
-      h.tw[k1 * 32 + l] = v;
-      h.twT[l * 32 + k1] = v;
-      h.tws[sw(l, k1)] = v;
+      h.tw[k1 * 32 + l] = make_double2((double)cosl(ang), (double)sinl(ang));
     }
   for (int m = 0; m < 32; m++) {
     const long double ang = PI * (long double)m / 64.0L;
@@ -375,63 +237,36 @@ static int ensure_tables() {
   return g_status[dev];
 }
 
-// twiddle T(l, k1): from the shared-memory copy (`sm`) or the global tables
-__device__ __forceinline__ double2 tw_fwd(const double2 *sm, int l, int k1) {  // lane = l
-#if SZ_TW_SMEM
-  return sm[sw(l, k1)];
-#else
-  (void)sm;
-  return __ldg(&g_t32.tw[k1 * 32 + l]);
-#endif
-}
-__device__ __forceinline__ double2 tw_inv(const double2 *sm, int l, int k1) {  // lane = k1
-#if SZ_TW_SMEM
-  return sm[sw(l, k1)];
-#else
-  (void)sm;
-  return __ldg(&g_t32.twT[l * 32 + k1]);
-#endif
-}
+// twiddle T(l = lane, k1) from the global (L1-resident) table
+__device__ __forceinline__ double2 tw_fwd(int l, int k1) { return __ldg(&g_t32.tw[k1 * 32 + l]); }
 
 // Forward transform of one warp. In: x[m] = (a_j + i a_{j+1024}) at j = lane + 32 m.
-// Out: x[k2] = spectrum at index lane + 32 k2 ("slot" order). `tsm` = shared twiddle copy (SZ_TW_SMEM).
-__device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, const double2 *tsm, int lane) {
-#if SZ_TAN_TWIST & 1
-  twist_all_unscaled<false, 1>(x);
-  dft32_scaled<false>(x);  // x[k1] = B[l = lane][k1]
-#else
+// Out: x[k2] = spectrum at index lane + 32 k2 ("slot" order).
+__device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, int lane) {
 #pragma unroll
   for (int m = 1; m < 32; m++) x[m] = cmul(x[m], c_twist32[m]);
   dft32<false>(x);  // x[k1] = B[l = lane][k1]
-#endif
   __syncwarp();     // earlier readers of buf are done
 #pragma unroll
-  for (int k1 = 0; k1 < 32; k1++) buf[sw(lane, k1)] = cmul(x[k1], tw_fwd(tsm, lane, k1));
+  for (int k1 = 0; k1 < 32; k1++) buf[sw(lane, k1)] = cmul(x[k1], tw_fwd(lane, k1));
   __syncwarp();
 #pragma unroll
   for (int l = 0; l < 32; l++) x[l] = buf[sw(l, lane)];  // thread k1 = lane, natural l
   dft32<false>(x);                                        // x[k2] = Z[lane + 32 k2]
 }
 
-// Inverse transform (unnormalised). In: slot order. Out: x[m] = M (c_j + i c_{j+1024}), j = lane + 32 m;
-// with UNTWIST = false the final conj(w^{32m}) is left to the caller (untwist_round).
-template <bool UNTWIST = true>
-__device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, const double2 *tsm, int lane) {
+// Inverse transform (unnormalised). In: slot order. Out: x[m] = M (c_j + i c_{j+1024}) w^{32 m},
+// j = lane + 32 m, i.e. before the final untwist conj(w^{32m}) (done by the caller:
+// untwist_round fuses it with the exact rounding; UNTWIST = true applies it here).
+template <bool UNTWIST>
+__device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, int lane) {
   dft32<true>(x);  // x[l] = 32 B'[l][k1 = lane]
   __syncwarp();
-#if SZ_INV_TW_POST
 #pragma unroll
   for (int l = 0; l < 32; l++) buf[sw(l, lane)] = x[l];
   __syncwarp();
 #pragma unroll
-  for (int k1 = 0; k1 < 32; k1++) x[k1] = cmulc(buf[sw(lane, k1)], tw_fwd(tsm, lane, k1));  // thread l = lane
-#else
-#pragma unroll
-  for (int l = 0; l < 32; l++) buf[sw(l, lane)] = cmulc(x[l], tw_inv(tsm, l, lane));
-  __syncwarp();
-#pragma unroll
-  for (int k1 = 0; k1 < 32; k1++) x[k1] = buf[sw(lane, k1)];  // thread l = lane, natural k1
-#endif
+  for (int k1 = 0; k1 < 32; k1++) x[k1] = cmulc(buf[sw(lane, k1)], tw_fwd(lane, k1));  // thread l = lane
   dft32<true>(x);  // x[m] = M z_{lane + 32 m} w^{32 m}
   if constexpr (UNTWIST) {
 #pragma unroll
@@ -464,6 +299,15 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
                "l"(src), "r"(bytes), "r"(smem_u32(mbar))
                : "memory");
 }
+// release this warp's reads of the stage and count it; returns the previous count.
+// (__syncwarp orders the other lanes' reads before lane 0's release; the
+// last warp's acquire then orders every warp's reads before its async-proxy
+// fence and the bulk copy that overwrites the stage.)
+__device__ __forceinline__ uint32_t stage_release(uint32_t *ctr) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_u32(ctr)) : "memory");
+  return old;
+}
 
 // ------------------------------------------------------------------ kernel
 struct Args {
@@ -481,7 +325,6 @@ __host__ __device__ constexpr size_t abar_bytes(int n) { return ((size_t)n * 2 +
 __host__ __device__ constexpr size_t smem_bytes(int n) {
   return 8 * (size_t)kXbuf * sizeof(double2)  // per-warp transposition buffers (also the ACC copy)
          + 4 * (size_t)kM * sizeof(double2)  // BSK stage: one (i, limb), [o][row][32][32]
-         + (SZ_TW_SMEM ? (size_t)kXbuf * sizeof(double2) : 0)  // twiddle table copy
          + kCts * abar_bytes(n)              // modswitched masks
          + 16;                               // mbarrier
 }
@@ -491,73 +334,41 @@ __device__ __forceinline__ u64 acc_init(const u64 *v, int j, int bt, int g) {
   const u64 vv = (idx < kN) ? v[idx] : (u64)0 - v[idx - kN];
   return g ? vv : 0ull;
 }
-#ifndef SZ_PERSIST
-#define SZ_PERSIST 1  // one grid-stride launch instead of one launch per resident wave
-#endif
-#ifndef SZ_PUB_FUSED
-#define SZ_PUB_FUSED 0  // last limb also writes the rotation copy: correct, measured -25 % (codegen)
-#endif
-#ifndef SZ_D_ST32
-#define SZ_D_ST32 0  // 32-column TMEM stores of the digit spectra
-#endif
-#ifndef SZ_ACC_CQ
-#define SZ_ACC_CQ 4  // ACC coefficients m per TMEM access chunk (4: 16 columns, 8: 32 columns; sweep 2 (profiles/r01_warp_variants2.txt): 4 is 3 % faster with the current kernel)
-#endif
-constexpr int kCQ = SZ_ACC_CQ, kNC = 32 / SZ_ACC_CQ;
-// ACC chunk cc (4 kCQ columns) = coefficients j = lane + 32 m + 1024 h, m = kCQ cc + q (q < kCQ), h < 2
-template <int CQ = kCQ>
-__device__ __forceinline__ void acc_ld(uint32_t ta, int cc, u64 (&a)[CQ][2]) {
-  uint32_t r[4 * CQ];
-  if constexpr (CQ == 8) {
-    tmem_ld32(ta + 32 * cc, r);
-    tmem_wait_ld32(r);
-  } else {
-    tmem_ld16(ta + 16 * cc, r);
-    tmem_wait_ld16(r);
-  }
+// ACC chunk cc (16 TMEM columns) = coefficients j = lane + 32 m + 1024 h, m = kCQ cc + q (q < kCQ), h < 2
+// (16-column chunks measured 3 % faster than 32, profiles/r01_warp_variants2.txt)
+constexpr int kCQ = 4, kNC = 32 / kCQ;
+__device__ __forceinline__ void acc_ld(uint32_t ta, int cc, u64 (&a)[kCQ][2]) {
+  uint32_t r[4 * kCQ];
+  tmem_ld16(ta + 16 * cc, r);
+  tmem_wait_ld16(r);
 #pragma unroll
-  for (int q = 0; q < CQ; q++)
+  for (int q = 0; q < kCQ; q++)
 #pragma unroll
     for (int h = 0; h < 2; h++) a[q][h] = (u64)r[4 * q + 2 * h] | ((u64)r[4 * q + 2 * h + 1] << 32);
 }
-template <int CQ = kCQ>
-__device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[CQ][2]) {
-  uint32_t r[4 * CQ];
+__device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[kCQ][2]) {
+  uint32_t r[4 * kCQ];
 #pragma unroll
-  for (int q = 0; q < CQ; q++)
+  for (int q = 0; q < kCQ; q++)
 #pragma unroll
     for (int h = 0; h < 2; h++) {
       r[4 * q + 2 * h] = (uint32_t)a[q][h];
       r[4 * q + 2 * h + 1] = (uint32_t)(a[q][h] >> 32);
     }
-  if constexpr (CQ == 8) tmem_st32(ta + 32 * cc, r);
-  else tmem_st16(ta + 16 * cc, r);
+  tmem_st16(ta + 16 * cc, r);
 }
 
-// bits of x + 1.5 * 2^52: round(x) + bits(1.5 * 2^52) for |x| < 2^51 (see rint_small)
-__device__ __forceinline__ u64 limb_bits(double x) { return (u64)__double_as_longlong(x + 6755399441055744.0); }
 constexpr u64 kMagicBits = 0x4338000000000000ull;  // bits of 1.5 * 2^52
-constexpr u64 kLimbOffset3 = kMagicBits + (kMagicBits << 22) + (kMagicBits << 44);  // sum_p bits(M) << 22 p
-
-#ifndef SZ_ROUND_SYNC
-#define SZ_ROUND_SYNC 0  // W > 0: a CTA starts round r only after every CTA finished round r - W. Measured at 131 072
-                         // (tools/ab_roundsync.sh): W = 1 cuts DRAM reads 56x (1.87 TB -> 34 GB per launch) but is
-                         // 28 % slower (all CTAs hammer the same BSK lines in L2); W = 2: 1.8x fewer reads, 14 % slower.
-                         // The drifting persistent grid is FP64-bound with HBM at ~10 % of its bandwidth, so 0.
-#endif
-#if SZ_ROUND_SYNC
-__device__ unsigned int g_round_done;
-#endif
 
 template <int P>
 __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t tmem_slot;
+  __shared__ uint32_t mac_done;  // warps finished with the staged limb, monotone (the 8th of a round re-arms)
   const int n = A.n, w = A.w, blog = A.base_log;
   double2 *xbuf_all = reinterpret_cast<double2 *>(smem);
   double2 *gbuf = xbuf_all + 8 * kXbuf;
-  double2 *tsm = gbuf + 4 * kM;  // twiddle copy (SZ_TW_SMEM)
-  unsigned char *abar_base = reinterpret_cast<unsigned char *>(tsm + (SZ_TW_SMEM ? kXbuf : 0));
+  unsigned char *abar_base = reinterpret_cast<unsigned char *>(gbuf + 4 * kM);
   uint64_t *mbar = reinterpret_cast<uint64_t *>(abar_base + kCts * abar_bytes(n));
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
   const int cs = wid & 3, g = wid >> 2;  // ciphertext slot, GLWE component
@@ -567,9 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
 
   if (wid == 0) tmem_alloc(&tmem_slot, kTmemCols);
   if (tid == 32) mbar_init(mbar, 1);
-#if SZ_TW_SMEM
-  for (int e = tid; e < kXbuf; e += kThreads) tsm[e] = g_t32.tws[e];
-#endif
+  if (tid == 0) mac_done = 0;
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
@@ -581,26 +390,9 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   };
   uint32_t round = 0;  // completed bulk copies (mbarrier phase parity)
   const u64 half_q = 1ull << (63 - blog);
-  __shared__ int mac_done;  // warps finished with the staged limb (the last one re-arms the stage)
-  if (tid == 0) mac_done = 0;
 
   const long ngroups = (A.count + kCts - 1) / kCts;
-  long round_no = 0;
-  for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x, round_no++) {
-#if SZ_ROUND_SYNC
-    if (round_no >= SZ_ROUND_SYNC) {
-      if (tid == 0) {
-        const unsigned need = (unsigned)((round_no - SZ_ROUND_SYNC + 1) * gridDim.x);
-        unsigned v;
-        for (;;) {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&g_round_done) : "memory");
-          if (v >= need) break;
-          __nanosleep(256);
-        }
-      }
-      __syncthreads();
-    }
-#endif
+  for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     if (tid == 0) issue(0, P - 1);
     const long c_raw = grp * kCts + cs;
     const bool live = c_raw < A.count;
@@ -621,10 +413,6 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
 #pragma unroll
         for (int h = 0; h < 2; h++) a4[q][h] = acc_init(v, lane + 32 * (kCQ * cc + q) + 1024 * h, bt, g);
       acc_st(ta_acc, cc, a4);
-#if SZ_PUB_FUSED
-#pragma unroll
-      for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
-#endif
     }
     tmem_wait_st();
     __syncthreads();  // abar visible
@@ -633,7 +421,6 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
       const int a = abar[i];
       // ---------------- publish ACC_g for the rotation, as coefficient pairs
       // accp[s] = (ACC_g[s], ACC_g[s + 1024]), s < 1024 (one 16-byte access serves both h)
-#if !SZ_PUB_FUSED
       __syncwarp();  // previous inverse FFT's readers of xbuf are done
 #pragma unroll
       for (int cc = 0; cc < kNC; cc++) {
@@ -642,7 +429,6 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
 #pragma unroll
         for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
       }
-#endif
       __syncwarp();
       // ---------------- digits of X^a ACC_g - ACC_g (a4.1-a4.2), forward FFT
       // (X^a ACC)[j] = +-ACC[(j - a) mod 2N]: for j0 = lane + 32 m and j1 = j0 + 1024,
@@ -668,28 +454,18 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
                                          (double)((i64)(r1 - a4[q][1] + half_q) >> (64 - blog)));
         }
       }
-      fwd_fft32(x, xbuf, tsm, lane);
+      fwd_fft32(x, xbuf, lane);
       if (i > 0) {  // both warps of the ciphertext are past the previous CMux's MACs (D^ reads)
         tmem_fence_before();
         asm volatile("bar.sync %0, %1;" ::"r"(5 + cs), "r"(64) : "memory");
         tmem_fence_after();
       }
-#if SZ_D_ST32
-#pragma unroll
-      for (int jj = 0; jj < 4; jj++) {
-        uint32_t r32[32];
-        pack4(&x[8 * jj], *reinterpret_cast<uint32_t(*)[16]>(&r32[0]));
-        pack4(&x[8 * jj + 4], *reinterpret_cast<uint32_t(*)[16]>(&r32[16]));
-        tmem_st32(ta_dg + 32 * jj, r32);
-      }
-#else
 #pragma unroll
       for (int jj = 0; jj < 8; jj++) {
         uint32_t r16[16];
         pack4(&x[4 * jj], r16);
         tmem_st16(ta_dg + 16 * jj, r16);
       }
-#endif
       tmem_wait_st();
       tmem_fence_before();
       asm volatile("bar.sync %0, %1;" ::"r"(1 + cs), "r"(64) : "memory");  // D^_0 and D^_1 written
@@ -702,7 +478,6 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
         double2 y[32];
         const double2 *G0 = gbuf + (size_t)(2 * g) * kM + lane;  // [o = g][row 0]
         const double2 *G1 = G0 + kM;                             // [o = g][row 1]
-#if SZ_MAC_X32
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) {
           uint32_t d0[32], d1[32];
@@ -718,83 +493,35 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
             y[r] = acc;
           }
         }
-#else
-#pragma unroll
-        for (int jj = 0; jj < 8; jj++) {
-          uint32_t d0[16], d1[16];
-          tmem_ld16(ta_d0 + 16 * jj, d0);
-          tmem_ld16(ta_d1 + 16 * jj, d1);
-          tmem_wait_ld16x2(d0, d1);
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const int r = 4 * jj + q;
-            double2 acc = make_double2(0.0, 0.0);
-            cmac(acc, unpack1(d0, q), G0[r * 32]);
-            cmac(acc, unpack1(d1, q), G1[r * 32]);
-            y[r] = acc;
-          }
-        }
-#endif
-        // this warp is done with the stage; the last of the 8 warps re-arms it
+        // this warp is done with the stage; the 8th warp of the round re-arms it
         // with the next (i, limb) -- no CTA-wide barrier
         __syncwarp();
-        if (lane == 0) {
-          if (atomicAdd(&mac_done, 1) == kThreads / 32 - 1) {
-            mac_done = 0;
-            if (p > 0) issue(i, p - 1);
-            else if (i + 1 < n) issue(i + 1, P - 1);
-          }
+        if (lane == 0 && (stage_release(&mac_done) & 7) == 7) {
+          if (p > 0) issue(i, p - 1);
+          else if (i + 1 < n) issue(i + 1, P - 1);
         }
-        constexpr bool kFusedUntwist = (SZ_TAN_TWIST & 2) && SZ_ACC_FAST == 2 && P == 3;
-        inv_fft32<!kFusedUntwist>(y, xbuf, tsm, lane);
-        // sum_p bits(M) << p w, removed once per CMux (SZ_ACC_FAST == 2)
+        constexpr bool kFusedUntwist = (P == 3);
+        inv_fft32<!kFusedUntwist>(y, xbuf, lane);
+        // P = 3: bits(x + 1.5 2^52) << 22p per limb, the magic constant's share of
+        // all three limbs removed once per CMux (at p = 0)
         const u64 limb_off = (p == 0) ? kMagicBits + (kMagicBits << w) + (kMagicBits << (2 * w)) : 0ull;
-#if SZ_PUB_FUSED
-        if (p == 0) __syncwarp();  // the last limb also publishes the new ACC into xbuf
-#endif
 #pragma unroll
         for (int cc = 0; cc < kNC; cc++) {
           u64 a4[kCQ][2];
           acc_ld(ta_acc, cc, a4);
 #pragma unroll
           for (int q = 0; q < kCQ; q++) {
-            if (kFusedUntwist) {
+            if constexpr (kFusedUntwist) {
               u64 bx, by;
               untwist_round(y[kCQ * cc + q], kCQ * cc + q, bx, by);
               a4[q][0] += (bx << (p * w)) - limb_off;
               a4[q][1] += (by << (p * w)) - limb_off;
-            } else if (SZ_ACC_FAST == 2 && P == 3) {
-              // branch-free: bits(x + M) << 22p, the magic constant's share removed at p = 0
-              a4[q][0] += (limb_bits(y[kCQ * cc + q].x) << (p * w)) - limb_off;
-              a4[q][1] += (limb_bits(y[kCQ * cc + q].y) << (p * w)) - limb_off;
-            } else if (SZ_ACC_FAST == 1 && P == 3 && w == 22) {
-              // round(x) << 22p via the 1.5 * 2^52 trick; the magic constant's
-              // bits are removed once per CMux (kLimbOffset3, at p = 0)
-              if (p == 2) {
-                a4[q][0] += (u64)((uint32_t)limb_bits(y[kCQ * cc + q].x) << 12) << 32;
-                a4[q][1] += (u64)((uint32_t)limb_bits(y[kCQ * cc + q].y) << 12) << 32;
-              } else if (p == 1) {
-                a4[q][0] += limb_bits(y[kCQ * cc + q].x) << 22;
-                a4[q][1] += limb_bits(y[kCQ * cc + q].y) << 22;
-              } else {
-                a4[q][0] += limb_bits(y[kCQ * cc + q].x) - kLimbOffset3;
-                a4[q][1] += limb_bits(y[kCQ * cc + q].y) - kLimbOffset3;
-              }
-            } else if (P == 3) {
-              a4[q][0] += rint_small(y[kCQ * cc + q].x) << (p * w);
-              a4[q][1] += rint_small(y[kCQ * cc + q].y) << (p * w);
             } else {
               a4[q][0] += limb_to_torus(y[kCQ * cc + q].x, p, P, w);
               a4[q][1] += limb_to_torus(y[kCQ * cc + q].y, p, P, w);
             }
           }
           acc_st(ta_acc, cc, a4);
-#if SZ_PUB_FUSED
-          if (p == 0) {
-#pragma unroll
-            for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
-          }
-#endif
         }
         tmem_wait_st();
       }
@@ -821,9 +548,6 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
       }
     }
     __syncthreads();  // abar reuse
-#if SZ_ROUND_SYNC
-    if (tid == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&g_round_done) : "memory");
-#endif
   }
   tmem_fence_before();
   __syncthreads();
@@ -840,12 +564,7 @@ struct B2FArgs {
 // one warp per (i, row, o, p)
 __global__ void __launch_bounds__(32) bsk_to_fourier_warp_kernel(B2FArgs A) {
   __shared__ __align__(16) double2 buf[kXbuf];
-  __shared__ __align__(16) double2 tsm[SZ_TW_SMEM ? kXbuf : 1];
   const int lane = threadIdx.x;
-#if SZ_TW_SMEM
-  for (int e = lane; e < kXbuf; e += 32) tsm[e] = g_t32.tws[e];
-  __syncwarp();
-#endif
   long blk = blockIdx.x;
   const int p = blk % A.P; blk /= A.P;
   const int o = blk % 2; blk /= 2;
@@ -860,7 +579,7 @@ __global__ void __launch_bounds__(32) bsk_to_fourier_warp_kernel(B2FArgs A) {
     limb_split(gsrc[lane + 32 * m + 1024], A.P, A.w, l1);
     x[m] = make_double2(l0[p], l1[p]);
   }
-  fwd_fft32(x, buf, tsm, lane);
+  fwd_fft32(x, buf, lane);
   double2 *dst = A.fbsk + ((((size_t)i * A.P + p) * 2 + o) * 2 + row) * kM;
   const double scale = 1.0 / kM;
 #pragma unroll
@@ -882,11 +601,7 @@ long blind_rotate_warp_wave() {
   return (long)sms * w32::kCts;  // one CTA (4 ciphertexts) per SM: 512 TMEM columns each
 }
 
-long blind_rotate_warp_launches(size_t count) {
-  const long wave = blind_rotate_warp_wave();
-  if (wave <= 0) return -1;
-  return SZ_PERSIST ? (count ? 1 : 0) : (long)((count + wave - 1) / wave);
-}
+long blind_rotate_warp_launches(size_t count) { return count ? 1 : 0; }
 
 int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
                              const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
@@ -913,35 +628,16 @@ int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64
   SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long wave = blind_rotate_warp_wave();
   if (wave <= 0) return SILENZIO_ERR_CUDA;
-  if (SZ_PERSIST) {
-    // one persistent launch, CTA b handles groups b, b + grid, ... (grid-stride).
-    // CTAs drift apart in i over a long batch, but the bulk-copy stage prefetch
-    // tolerates the resulting L2 misses: measured +3.8 % at 131 072 ciphertexts
-    // over one launch per resident wave (which kept every CTA on the same BSK_i)
-    const long groups = ((long)count + w32::kCts - 1) / w32::kCts;
-    const long grid = groups < wave / w32::kCts ? groups : wave / w32::kCts;
-#if SZ_ROUND_SYNC
-    {
-      void *ctr = nullptr;
-      SZ_CUDA_OK(cudaGetSymbolAddress(&ctr, w32::g_round_done));
-      SZ_CUDA_OK(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream));
-    }
-#endif
-    kern<<<(unsigned)grid, w32::kThreads, smem, stream>>>(A);
-    SZ_LAUNCH_OK();
-    return SILENZIO_OK;
-  }
-  // one launch per resident wave (every CTA sweeps BSK_0..BSK_{n-1} together)
-  for (long c0 = 0; c0 < (long)count; c0 += wave) {
-    w32::Args W = A;
-    const long cnt = ((long)count - c0 < wave) ? (long)count - c0 : wave;
-    W.lwe_small = A.lwe_small + (size_t)c0 * (A.n + 1);
-    W.lut_ids = A.lut_ids ? A.lut_ids + c0 : nullptr;
-    W.lwe_out = A.lwe_out + (size_t)c0 * (w32::kN + 1);
-    W.count = cnt;
-    kern<<<(unsigned)((cnt + w32::kCts - 1) / w32::kCts), w32::kThreads, smem, stream>>>(W);
-    SZ_LAUNCH_OK();
-  }
+  // one persistent launch, CTA b handles groups b, b + grid, ... (grid-stride).
+  // CTAs drift apart in i over a long batch, but the bulk-copy stage prefetch
+  // tolerates the resulting L2 misses: measured +3.8 % at 131 072 ciphertexts
+  // over one launch per resident wave (which kept every CTA on the same BSK_i);
+  // lock-step rounds of the grid (fewer DRAM re-reads) measured 14-28 % slower
+  // (DESIGN.md §8).
+  const long groups = ((long)count + w32::kCts - 1) / w32::kCts;
+  const long grid = groups < wave / w32::kCts ? groups : wave / w32::kCts;
+  kern<<<(unsigned)grid, w32::kThreads, smem, stream>>>(A);
+  SZ_LAUNCH_OK();
   return SILENZIO_OK;
 }
 

@@ -9,6 +9,7 @@ import ctypes
 import os
 from dataclasses import dataclass
 
+import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -75,6 +76,8 @@ def load():
         "silenzio_relu_cap": ([V, S, ctypes.c_int32, V, V, V, P, V, S, V], I),
         "silenzio_relu_mask": ([V, V, S, ctypes.c_int32, V, V, V, P, V, S, V], I),
         "silenzio_weight_update": ([V, V, S, ctypes.c_int32, ctypes.c_int32, V, V, V, P, V, S, V], I),
+        "silenzio_pbs_trace_begin": ([I, V, S, ctypes.c_uint64, ctypes.c_uint64, S, S, S], I),
+        "silenzio_pbs_trace_end": ([I, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_long),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -97,7 +100,7 @@ def exported_symbols():
         "silenzio_mrns_combine_workspace_bytes", "silenzio_mrns_digit_combine",
         "silenzio_shift2msbs_workspace_bytes", "silenzio_shift2msbs_pm",
         "silenzio_train_workspace_bytes", "silenzio_channel16", "silenzio_rns_sign3", "silenzio_relu_cap",
-        "silenzio_relu_mask", "silenzio_weight_update",
+        "silenzio_relu_mask", "silenzio_weight_update", "silenzio_pbs_trace_begin", "silenzio_pbs_trace_end",
     ]
 
 
@@ -459,3 +462,38 @@ def shift2msbs_pm(residues, moduli, w, gamma, keys_a, Pa, keys_b, Pb, ksk_ab, pa
         _ptr(keys_a["ksk"]), ctypes.byref(pa), _ptr(keys_b["fbsk"]), ctypes.byref(pb), _ptr(ksk_ab),
         ctypes.byref(pab), _ptr(ksk_ba), ctypes.byref(pba), _ptr(ws), ws.numel(), _stream(stream)))
     return out, mb
+
+
+# ------------------------------------------------------------ sampled-PBS trace
+class PbsTrace:
+    """Context manager around silenzio_pbs_trace_begin/end: records every
+    `stride`-th PBS element the gadget drivers evaluate (kind 0: set-A PBS,
+    kind 1: set-B blind rotation + SE) into a device tensor of records
+    [input | output | test polynomial | global index, lut id] (u64 words).
+    After exit: .records [n][words] (int64 tensor), .seen = elements counted."""
+
+    def __init__(self, kind, max_records, stride, in_words, out_words, lut_words, device, phase=0):
+        self.kind, self.max, self.stride, self.phase = int(kind), int(max_records), int(stride), int(phase)
+        self.words = (int(in_words), int(out_words), int(lut_words))
+        self.buf = torch.zeros((self.max, sum(self.words) + 2), dtype=torch.int64, device=device)
+        self.records, self.seen = None, 0
+
+    def __enter__(self):
+        _check(load().silenzio_pbs_trace_begin(self.kind, _ptr(self.buf), self.max, self.stride, self.phase,
+                                               *self.words))
+        return self
+
+    def __exit__(self, *exc):
+        seen = ctypes.c_uint64(0)
+        n = load().silenzio_pbs_trace_end(self.kind, ctypes.byref(seen))
+        if n < 0:
+            _check(n)
+        torch.cuda.synchronize()
+        self.records, self.seen = self.buf[:n], int(seen.value)
+        return False
+
+    def split(self):
+        """(inputs, outputs, test polynomials, global indices, lut ids) as host u64 / int arrays."""
+        r = self.records.cpu().numpy().view(np.uint64)
+        a, b, c = self.words
+        return r[:, :a], r[:, a:a + b], r[:, a + b:a + b + c], r[:, -2].astype(np.int64), r[:, -1].astype(np.int64)

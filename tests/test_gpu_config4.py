@@ -100,50 +100,5 @@ def test_config4_tiny_gpu_vs_oracle(dev):
     assert maxbit - (GAMMA_SIGNED - 1) == shift
 
 
-@pytest.mark.skipif(os.environ.get("SILENZIO_FULL") != "1",
-                    reason="~10 min on one B200 (53k set-B PBS); run with SILENZIO_FULL=1 (profiles/r01_config4_full.json)")
-def test_config4_full_size(dev):
-    """Activations X(64x784) W(784x128) and logits A'(64x128) W'(128x10) as RNS
-    residues (set A, n = 742); Shift2MSBs+- to Gamma = 4 of both through the 8-bit
-    stage (set B, n = 1024, N = 32768); CE gradient of the scaled logits."""
-    from paper_2504_17785_b200 import silenzio, workload as wl
-    from synth import streams
-    PA, PB = get_params("A"), get_params("B")
-    t0 = time.perf_counter()
-    g, _ = gpu_setup(PA, PB, 83, dev, False)
-    torch.cuda.synchronize()
-    t_keys = time.perf_counter() - t0
-    rng = streams(83)["messages"]
-    X, W = rng.integers(-8, 8, size=(64, 784)), rng.integers(-8, 8, size=(784, 128))
-    A2, W2 = rng.integers(-8, 8, size=(64, 128)), rng.integers(-8, 8, size=(128, 10))
-    key = g["ka"]["big_key"]
-    dec = lambda t: wl.decode(wl.to_host_u64(silenzio.lwe_phase_batch(t.reshape(-1, PA.big_dim + 1), key)), PA.p)  # noqa: E731
-    report = {"workload": "configs[4]: Shift2MSBs+- (Gamma=4) of 64x128 activations and 64x10 logits via the "
-                          "8-bit stage + CE gradient", "keygen_s": t_keys}
-    scaled = {}
-    for name, T in (("activations", X @ W), ("logits", A2 @ W2)):
-        res = G.to_rns(T.reshape(-1), BASE6)
-        r = lwe_randomness(PA, res.size, 84)
-        ct = wl.encrypt(PA, res.reshape(-1), r, key, dev).reshape(len(BASE6), res.shape[1], -1)
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        Y, mb, _, _, _ = gpu_shift2msbs(g, ct, PA, PB)
-        torch.cuda.synchronize()
-        report[name + "_s"] = time.perf_counter() - t1
-        ref, shift = G.shift2msbs_pm(res, BASE6, W_BITS, GAMMA_SIGNED)
-        got = G.signed_decode(dec(Y), 32)
-        report[name + "_mismatches"] = int((got != ref).sum())
-        assert np.array_equal(got, ref), name
-        scaled[name] = (Y, ref)
-    Y, ref = scaled["logits"]
-    lab = np.zeros((64, 10), dtype=np.int64)
-    lab[np.arange(64), rng.integers(0, 10, size=64)] = 1
-    rl = lwe_randomness(PA, 640, 85)
-    yl = wl.encrypt(PA, lab.reshape(-1), rl, key, dev).reshape(64, 10, -1)
-    ce = silenzio.int_ce_grad(Y.reshape(64, 10, -1).contiguous(), yl, g["ka"]["fbsk"], g["ka"]["ksk"], PA)
-    got = G.signed_decode(dec(ce).reshape(64, 10), 32)
-    assert np.array_equal(got, G.int_ce_loss_deriv(ref.reshape(64, 10), lab, 3, 0))
-    os.makedirs("gpurun_out", exist_ok=True)
-    with open("gpurun_out/config4.json", "w") as f:
-        json.dump(report, f)
-    print(json.dumps(report))
+# The full-size configs[4] run (every element vs Alg. 3/4/5, plus traced oracle
+# replays of its set-A and set-B PBS) is tests/test_gpu_replays.py.

@@ -1,0 +1,249 @@
+"""Full-parameter oracle replays of BASELINE configs[1]-[4] (SURVEY.md §8(d)
+"Oracle beside it"), on identical inputs, phase within 2^-32 (BJ north_star):
+
+  config 1  the bench's launch configuration at batch 131 072: 256 sampled PBS
+  config 2  set C, 16 384 ciphertexts, x mod 7 then y^2 mod 64: every output
+            decrypts; 32 PBS of each stage replayed (schoolbook N = 8192)
+  config 3  one row of the 16x784 . 784x64 Matmul^RNS (base {5,..,16}, the
+            driver's own PBS sequence): CRT = X W on every output, and 1 024
+            of the driver's PBS (sampled by silenzio_pbs_trace) replayed
+  config 4  Shift2MSBs+- (Gamma = 4) of the 64x128 activations and 64x10
+            logits through the 8-bit stage + the CE gradient: every element
+            equals the cleartext Alg. 3/4/5; 256 sampled set-A PBS and 4 sampled
+            set-B blind rotations (n = 1024, N = 32768) replayed
+
+The replays run on a background thread (the oracle uses every host core)
+while the next test keeps the GPU busy; test_zz_collect_replays waits for all
+of them and asserts the phase bound (so this file must run in order)."""
+import concurrent.futures as cf
+import json
+import math
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import gadgets as G
+from synth import (cross_ksk_randomness, get_params, key_randomness, lut_ids, lut_tables, lwe_randomness,
+                   messages, streams)
+
+pytestmark = pytest.mark.gpu
+PHASE_TOL = 2 ** 32
+BASE6 = [5, 7, 9, 11, 13, 16]
+_POOL = cf.ThreadPoolExecutor(max_workers=1)
+_JOBS = []      # (name, future -> (max |dphi|, count, seconds))
+_REPORT = {}
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required")
+    return torch.device("cuda:0")
+
+
+def u64(t):
+    return t.detach().cpu().numpy().view(np.uint64)
+
+
+def _phase_gap(got, ref, key):
+    return int(np.abs(oracle.torus_diff(oracle.lwe_phase(got, key), oracle.lwe_phase(ref, key))).max())
+
+
+def sample_idx(n, k, fixed, seed):
+    """k distinct indices in [0, n): the `fixed` ones (edges) plus seeded random picks."""
+    fixed = [int(f) for f in dict.fromkeys(fixed) if 0 <= f < n]
+    rest = np.setdiff1d(np.random.default_rng(seed).permutation(n)[:k + len(fixed)], fixed)[:k - len(fixed)]
+    return np.sort(np.concatenate([fixed, rest]).astype(np.int64))
+
+
+def submit(name, fn):
+    def job():
+        t0 = time.perf_counter()
+        d, n = fn()
+        return d, n, time.perf_counter() - t0
+    _JOBS.append((name, _POOL.submit(job)))
+
+
+def replay_set_a(name, P, okeys, cts, outs, polys):
+    """oracle.pbs of each traced (input, test polynomial) vs the GPU output."""
+    cts, outs, polys = np.ascontiguousarray(cts), np.ascontiguousarray(outs), np.ascontiguousarray(polys)
+
+    def fn():
+        ref = oracle.pbs(cts, np.arange(len(cts), dtype=np.uint32), polys, okeys["bsk"], okeys["ksk"], P)
+        return _phase_gap(outs, ref, okeys["big_key"]), len(cts)
+    submit(name, fn)
+
+
+def test_config2_full_chain_with_replays(dev):
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P = get_params("C")
+    rnd = key_randomness(P, 5)
+    ok, gk = oracle.keygen(P, rnd), wl.device_keys(P, rnd, dev)
+    cnt, per_stage = 16384, 32
+    tabs = np.array([[x % 7 for x in range(64)], [(y * y) % 64 for y in range(64)]])
+    lut = wl.luts_from_tables(tabs, P.p, P.N, dev)
+    m = messages(cnt, P.p, 5)
+    ct = wl.encrypt(P, m, lwe_randomness(P, cnt, 5), gk["big_key"], dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s1 = silenzio.pbs_batch(ct, torch.zeros(cnt, dtype=torch.int32, device=dev), lut, gk["fbsk"], gk["ksk"], P)
+    s2 = silenzio.pbs_batch(s1, torch.ones(cnt, dtype=torch.int32, device=dev), lut, gk["fbsk"], gk["ksk"], P)
+    torch.cuda.synchronize()
+    _REPORT["config2_gpu_s"] = time.perf_counter() - t0
+    dec = lambda t: wl.decode(u64(silenzio.lwe_phase_batch(t, gk["big_key"])), P.p)  # noqa: E731
+    assert np.array_equal(dec(s1), m % 7)
+    assert np.array_equal(dec(s2), (m % 7) ** 2 % 64)
+    # sample: first / last, wave edges of the 148-ciphertext waves, random picks
+    pick = sample_idx(cnt, per_stage, [0, 147, 148, cnt - 1], 55)
+    vs = np.stack([oracle.test_polynomial(oracle.encode(tabs[i], P.p), P.p, P.N) for i in range(2)])
+    ct_h, s1_h, s2_h = u64(ct)[pick], u64(s1)[pick], u64(s2)[pick]
+
+    def fn():
+        o1 = oracle.pbs(ct_h, np.zeros(len(pick), np.uint32), vs, ok["bsk"], ok["ksk"], P)
+        o2 = oracle.pbs(s1_h, np.ones(len(pick), np.uint32), vs, ok["bsk"], ok["ksk"], P)
+        return max(_phase_gap(s1_h, o1, ok["big_key"]), _phase_gap(s2_h, o2, ok["big_key"])), 2 * len(pick)
+    submit("config2 (set C, 32 per stage)", fn)
+
+
+def test_config1_full_batch_256_replays(dev):
+    """The bench's launch configuration (131 072 ciphertexts, one persistent
+    launch), 256 sampled PBS replayed."""
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P = get_params("A")
+    rnd = key_randomness(P, 11)
+    ok, gk = oracle.keygen(P, rnd), wl.device_keys(P, rnd, dev)
+    B = 131072
+    tabs = lut_tables(8, P.p, 11)
+    luts = wl.luts_from_tables(tabs, P.p, P.N, dev)
+    ids = lut_ids(B, 8, 11)
+    m = messages(B, P.p, 11)
+    ct = wl.encrypt(P, m, lwe_randomness(P, B, 11), gk["big_key"], dev)
+    out = silenzio.pbs_batch(ct, torch.from_numpy(ids.astype(np.int32)).to(dev), luts, gk["fbsk"], gk["ksk"], P)
+    dec = wl.decode(u64(silenzio.lwe_phase_batch(out, gk["big_key"])), P.p)
+    assert np.array_equal(dec, tabs[ids, m])
+    grid = 148 * 4   # ciphertexts per round of the persistent grid
+    pick = sample_idx(B, 256, [0, 1, grid - 1, grid, B - grid, B - 1], 12)
+    sel = torch.from_numpy(pick).to(dev)
+    vs = np.stack([oracle.test_polynomial(oracle.encode(tabs[i], P.p), P.p, P.N) for i in range(8)])
+    replay_set_a("config1 (131072 batch, 256 sampled)", P, ok, u64(ct[sel]), u64(out[sel]), vs[ids[pick]])
+
+
+def test_config3_row_through_driver_with_traced_replays(dev):
+    """Row 0 of configs[3] (1 x 784 . 784 x 64, all six moduli) through
+    silenzio_rns_matmul; 1 024 of its PBS (evenly strided over the whole
+    schedule) recorded by silenzio_pbs_trace and replayed."""
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P = get_params("A")
+    rnd = key_randomness(P, 3)
+    ok, gk = oracle.keygen(P, rnd), wl.device_keys(P, rnd, dev)
+    rng = streams(3)["messages"]
+    X, W = rng.integers(-8, 8, size=(16, 784))[:1], rng.integers(-8, 8, size=(784, 64))
+    a, b, c = X.shape[0], X.shape[1], W.shape[1]
+    Xc = wl.encrypt(P, X.reshape(-1), lwe_randomness(P, a * b, 301), gk["big_key"], dev).reshape(a, b, -1)
+    Wc = wl.encrypt(P, W.reshape(-1), lwe_randomness(P, b * c, 302), gk["big_key"], dev).reshape(b, c, -1)
+    n_rec, approx_total = 1024, 1_440_000   # PBS of one row (~22.9 M for 16 rows)
+    stride = approx_total // n_rec
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    with silenzio.PbsTrace(0, n_rec, stride, P.big_dim + 1, P.big_dim + 1, P.N, dev) as tr:
+        out = silenzio.rns_matmul(Xc, Wc, BASE6, gk["fbsk"], gk["ksk"], P)
+        torch.cuda.synchronize()
+    _REPORT["config3_row_gpu_s"] = time.perf_counter() - t0
+    _REPORT["config3_row_pbs"] = tr.seen
+    ph = u64(silenzio.lwe_phase_batch(out.reshape(-1, P.big_dim + 1), gk["big_key"])).reshape(len(BASE6), a, c)
+    from oracle.fhe_gadgets import decode_residues
+    res = decode_residues(ph, BASE6)
+    assert np.array_equal(G.signed_decode(G.crt(res, BASE6), math.prod(BASE6)), X @ W)
+    cts, outs, polys, gidx, _ = tr.split()
+    assert len(cts) >= min(n_rec, tr.seen // stride) and len(cts) > 0
+    assert np.all(np.diff(gidx) == stride)
+    replay_set_a(f"config3 row 0 ({len(cts)} traced of {tr.seen} PBS)", P, ok, cts, outs, polys)
+
+
+def test_config4_full_size_with_traced_replays(dev):
+    """configs[4] at full size (64x128 activations, 64x10 logits, set A n = 742
+    + the 8-bit stage at set B n = 1024, N = 32768): every output equals the
+    cleartext Alg. 3/4/5; 256 set-A PBS and 4 set-B blind rotations sampled
+    from the driver's own sequence and replayed."""
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    PA, PB = get_params("A"), get_params("B")
+    KS_AB, KS_BA = (4, 5), (10, 4)
+    seed = 83
+    t0 = time.perf_counter()
+    ra, rb = key_randomness(PA, seed), key_randomness(PB, seed + 1)
+    ka, kb = wl.device_keys(PA, ra, dev), wl.device_keys(PB, rb, dev)
+    rab = cross_ksk_randomness(PA.big_dim, KS_AB[1], PB.n, PB.lwe_sigma_log2, seed, 1)
+    rba = cross_ksk_randomness(PB.big_dim, KS_BA[1], PA.big_dim, PA.glwe_sigma_log2, seed, 2)
+    ksk_ab = silenzio.ksk_generate(ka["big_key"], kb["lwe_key"], wl.to_dev(rab["ksk_mask"], dev),
+                                   wl.to_dev(rab["ksk_noise"], dev), *KS_AB)
+    ksk_ba = silenzio.ksk_generate(kb["big_key"], ka["big_key"], wl.to_dev(rba["ksk_mask"], dev),
+                                   wl.to_dev(rba["ksk_noise"], dev), *KS_BA)
+    pab = silenzio.ks_params(PA.big_dim, PB.n, *KS_AB, like=PB)
+    pba = silenzio.ks_params(PB.big_dim, PA.big_dim, *KS_BA, like=PB)
+    torch.cuda.synchronize()
+    _REPORT["config4_keygen_s"] = time.perf_counter() - t0
+    rng = streams(seed)["messages"]
+    X, W = rng.integers(-8, 8, size=(64, 784)), rng.integers(-8, 8, size=(784, 128))
+    A2, W2 = rng.integers(-8, 8, size=(64, 128)), rng.integers(-8, 8, size=(128, 10))
+    key = ka["big_key"]
+    dec = lambda t: wl.decode(u64(silenzio.lwe_phase_batch(t.reshape(-1, PA.big_dim + 1), key)), PA.p)  # noqa: E731
+    # ~0.68 M set-A and ~53 k set-B PBS in the two Shift2MSBs+- calls (DESIGN §6b')
+    tra = silenzio.PbsTrace(0, 256, 2400, PA.big_dim + 1, PA.big_dim + 1, PA.N, dev)
+    trb = silenzio.PbsTrace(1, 4, 13249, PB.n + 1, PB.big_dim + 1, PB.N, dev, phase=777)
+    scaled = {}
+    with tra, trb:
+        for name, T in (("activations", X @ W), ("logits", A2 @ W2)):
+            res = G.to_rns(T.reshape(-1), BASE6)
+            ct = wl.encrypt(PA, res.reshape(-1), lwe_randomness(PA, res.size, 84), key, dev)
+            ct = ct.reshape(len(BASE6), res.shape[1], -1)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            Y, mb = silenzio.shift2msbs_pm(ct, BASE6, 4, 3, ka, PA, kb, PB, ksk_ab, pab, ksk_ba, pba)
+            torch.cuda.synchronize()
+            _REPORT[f"config4_{name}_s"] = time.perf_counter() - t1
+            ref, shift = G.shift2msbs_pm(res, BASE6, 4, 4)
+            got = G.signed_decode(dec(Y), 32)
+            _REPORT[f"config4_{name}_mismatches"] = int((got != ref).sum())
+            assert np.array_equal(got, ref), name
+            scaled[name] = (Y, ref)
+    Y, ref = scaled["logits"]
+    lab = np.zeros((64, 10), dtype=np.int64)
+    lab[np.arange(64), rng.integers(0, 10, size=64)] = 1
+    yl = wl.encrypt(PA, lab.reshape(-1), lwe_randomness(PA, 640, 85), key, dev).reshape(64, 10, -1)
+    ce = silenzio.int_ce_grad(Y.reshape(64, 10, -1).contiguous(), yl, ka["fbsk"], ka["ksk"], PA)
+    assert np.array_equal(G.signed_decode(dec(ce).reshape(64, 10), 32), G.int_ce_loss_deriv(ref.reshape(64, 10), lab, 3, 0))
+    _REPORT["config4_set_a_pbs"], _REPORT["config4_set_b_pbs"] = tra.seen, trb.seen
+    # oracle keys (bit-exact with the GPU keys: tests/test_gpu_parity.py, test_gpu_setb.py);
+    # the set-B oracle key (N = 32768 schoolbook) is generated inside its background job
+    oa = oracle.keygen(PA, ra)
+    cts, outs, polys, _, _ = tra.split()
+    assert len(cts) == 256
+    replay_set_a("config4 set A (256 traced)", PA, oa, cts, outs, polys)
+    sm, bo, bp, _, _ = trb.split()
+    assert len(sm) == 4
+
+    def fn():
+        ob = oracle.keygen(PB, rb)
+        ref_b = oracle.br_se(sm, np.arange(4, dtype=np.uint32), bp, ob["bsk"], PB)
+        return _phase_gap(bo, ref_b, ob["big_key"]), 4
+    submit("config4 set B (4 traced blind rotations, n = 1024, N = 32768)", fn)
+
+
+def test_zz_collect_replays():
+    """Wait for every background replay; each within 2^-32 of the GPU phase."""
+    rows = []
+    for name, fut in _JOBS:
+        d, n, secs = fut.result()
+        rows.append({"replay": name, "count": n, "max_abs_dphi": d, "oracle_s": secs})
+        print(f"{name}: {n} replayed, max |dphi| = {d} (2^{np.log2(max(d, 1)):.1f}), oracle {secs:.0f} s")
+    _REPORT["replays"] = rows
+    os.makedirs("gpurun_out", exist_ok=True)
+    with open("gpurun_out/replays.json", "w") as f:
+        json.dump(_REPORT, f, indent=1)
+    assert rows, "no replay jobs ran"
+    for r in rows:
+        assert r["max_abs_dphi"] <= PHASE_TOL, r
