@@ -54,7 +54,10 @@ typedef enum {
   SILENZIO_ERR_INVALID_PARAM = -1, /* inconsistent or out-of-range parameter */
   SILENZIO_ERR_UNSUPPORTED = -2,   /* valid TFHE parameters no kernel implements */
   SILENZIO_ERR_NULL_POINTER = -3,
-  SILENZIO_ERR_MISALIGNED = -4,    /* pointer not 16-byte aligned */
+  SILENZIO_ERR_MISALIGNED = -4,    /* pointer not aligned: 16 B for the Fourier BSK and workspaces
+                                      (vector / bulk-copy access), the element size (8 B u64, 4 B u32)
+                                      for ciphertext, LUT, KSK and id arrays (rows of k*N+1 words
+                                      cannot all be 16-byte aligned) */
   SILENZIO_ERR_COUNT = -5,         /* count = 0 where not allowed, or overflow */
   SILENZIO_ERR_WINDOW = -6,        /* gadget driver: value window larger than a PBS can evaluate */
   SILENZIO_ERR_CUDA = -7,          /* a CUDA launch / runtime call failed */
@@ -143,12 +146,16 @@ int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_i
  * memory recommended). Copies are chunked (`chunk` ciphertexts, 0 = auto) and
  * overlapped with compute on two internal streams created per call; the call
  * returns after the last output chunk has landed in host memory (synchronous).
- * workspace must hold silenzio_pbs_host_workspace_bytes(params, chunk). */
+ * workspace must hold silenzio_pbs_host_workspace_bytes(params, chunk).
+ * Ordering: the internal streams wait for the work already queued on `stream`
+ * (the stream that produced luts / fourier_bsk / ksk / workspace), so the
+ * caller needs no synchronisation before the call. */
 size_t silenzio_pbs_host_workspace_bytes(const silenzio_params *params, size_t chunk);
 int silenzio_pbs_batch_host(const uint64_t *lwe_in_host, const uint32_t *lut_ids_host,
                             const uint64_t *luts, uint32_t num_luts, const void *fourier_bsk,
                             const uint64_t *ksk, uint64_t *lwe_out_host, size_t count,
-                            size_t chunk, const silenzio_params *params, void *workspace);
+                            size_t chunk, const silenzio_params *params, void *workspace,
+                            void *stream);
 
 /* Linear LWE combination (PAPER.md l.101 linear ops):
  *  out[i] = sum_{t<terms} coef[i][t] * in[idx[i][t]] + (0,...,0,cst[i])  mod 2^64.

@@ -174,7 +174,9 @@ int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_i
   if (count == 0) return SILENZIO_OK;
   if (!lwe_small || !luts || !fbsk || !out) return SILENZIO_ERR_NULL_POINTER;
   if (num_luts == 0) return SILENZIO_ERR_INVALID_PARAM;
-  if (!sz_aligned16(fbsk)) return SILENZIO_ERR_MISALIGNED;
+  if (!sz_aligned16(fbsk) || !sz_aligned(lwe_small, 8) || !sz_aligned(out, 8) || !sz_aligned(luts, 8) ||
+      (lut_ids && !sz_aligned(lut_ids, 4)))
+    return SILENZIO_ERR_MISALIGNED;
   if (count > (1ull << 31)) return SILENZIO_ERR_COUNT;
   if (P->poly_size == 8192)
     return launch_blind_rotate_large(lwe_small, lut_ids, luts, num_luts, fbsk, out, count, P, sz_stream(stream));
@@ -194,6 +196,9 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
   if (P->ks_in_dim != P->glwe_dim * P->poly_size) return SILENZIO_ERR_INVALID_PARAM;
   if (count == 0) return SILENZIO_OK;
   if (!in || !luts || !fbsk || !ksk || !out) return SILENZIO_ERR_NULL_POINTER;
+  if (!sz_aligned(in, 8) || !sz_aligned(out, 8) || !sz_aligned(luts, 8) || !sz_aligned(ksk, 8) ||
+      (lut_ids && !sz_aligned(lut_ids, 4)))
+    return SILENZIO_ERR_MISALIGNED;
   if (count > (1ull << 31)) return SILENZIO_ERR_COUNT;  // the blind rotation's limit, checked before the keyswitch runs
   if (!workspace) return SILENZIO_ERR_WORKSPACE;
   if (in == out) return SILENZIO_ERR_INVALID_PARAM;
@@ -233,7 +238,7 @@ size_t silenzio_pbs_host_workspace_bytes(const silenzio_params *P, size_t chunk)
 
 int silenzio_pbs_batch_host(const uint64_t *in_h, const uint32_t *ids_h, const uint64_t *luts, uint32_t num_luts,
                             const void *fbsk, const uint64_t *ksk, uint64_t *out_h, size_t count, size_t chunk,
-                            const silenzio_params *P, void *workspace) {
+                            const silenzio_params *P, void *workspace, void *stream) {
   int st = check_params(P);
   if (st) return st;
   if (count == 0) return SILENZIO_OK;
@@ -251,6 +256,15 @@ int silenzio_pbs_batch_host(const uint64_t *in_h, const uint32_t *ids_h, const u
     return SILENZIO_ERR_CUDA;
   }
   int rc = SILENZIO_OK;
+  // The internal streams start after everything already queued on the
+  // caller's stream (keys, LUTs or workspace written there, or memory the
+  // caching allocator recycled), and the caller's stream is ordered after
+  // the last internal chunk before returning.
+  cudaEvent_t ready = nullptr;
+  if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(ready, sz_stream(stream)) != cudaSuccess ||
+      cudaStreamWaitEvent(s[0], ready, 0) != cudaSuccess || cudaStreamWaitEvent(s[1], ready, 0) != cudaSuccess)
+    rc = SILENZIO_ERR_CUDA;
   // Two stages alternate; each chunk: H2D in, PBS, D2H out on its stage's
   // stream, so chunk c+1's copies overlap chunk c's compute.
   for (size_t c0 = 0, it = 0; c0 < count && rc == SILENZIO_OK; c0 += chunk, it++) {
@@ -278,6 +292,7 @@ int silenzio_pbs_batch_host(const uint64_t *in_h, const uint32_t *ids_h, const u
     if (cudaStreamSynchronize(s[i]) != cudaSuccess) rc = SILENZIO_ERR_CUDA;
     cudaStreamDestroy(s[i]);
   }
+  if (ready) cudaEventDestroy(ready);
   return rc;
 }
 

@@ -25,6 +25,7 @@ typedef uint32_t u32;
 static inline cudaStream_t sz_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
 static inline bool sz_aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static inline bool sz_aligned(const void *p, uintptr_t bytes) { return (reinterpret_cast<uintptr_t>(p) & (bytes - 1)) == 0; }
 
 // Signed gadget decomposition (R3/R4): rounds a to
 // the top l*beta bits (half up), then extracts l balanced digits in [-B/2, B/2)

@@ -9,8 +9,9 @@
 // three access patterns bank-conflict free). ACC (2 x 8192 u64 = 128 KiB)
 // stays in shared memory. The (k+1)l = 4 digit spectra of a CMux are
 // thread-private (each thread's MAC reads exactly the slots its own forward
-// pass produced), so they live in per-thread local memory (L1/L2), with no
-// synchronisation and no workspace.
+// pass produced), so they live in this thread's lane of tensor memory (4 x 64
+// columns per lane quadrant, SZ_SETC_TMEM; the SZ_SETC_TMEM = 0 build keeps
+// them in per-thread local memory), with no synchronisation and no workspace.
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -1041,11 +1042,20 @@ static bool cluster_path(const silenzio_params *P) {
   return SZ_SETB_CLUSTER && P->pbs_level <= 2 && P->fft_limbs == 3 && brc_smem_bytes((int)P->lwe_dim) <= 227 * 1024;
 }
 
+// max co-resident clusters for (device, kernel, dynamic smem), cached (the
+// query is cheap but not free); guarded for concurrent host threads
 static long cluster_grid(const silenzio_params *P, void (*kern)(BRHArgs), size_t smem) {
-  static long cached[64] = {0};
+  struct Entry { int dev; void (*kern)(BRHArgs); size_t smem; long ncl; };
+  static std::mutex m;
+  static std::vector<Entry> cache;
+  (void)P;
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return -1;
-  if (cached[dev] > 0) return cached[dev];
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  {
+    std::lock_guard<std::mutex> lk(m);
+    for (const Entry &e : cache)
+      if (e.dev == dev && e.kern == kern && e.smem == smem) return e.ncl;
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kClQ * 64, 1, 1);
   cfg.blockDim = dim3(256, 1, 1);
@@ -1059,8 +1069,8 @@ static long cluster_grid(const silenzio_params *P, void (*kern)(BRHArgs), size_t
   cfg.numAttrs = 1;
   int ncl = 0;
   if (cudaOccupancyMaxActiveClusters(&ncl, (void *)kern, &cfg) != cudaSuccess || ncl <= 0) return -1;
-  (void)P;
-  cached[dev] = ncl;
+  std::lock_guard<std::mutex> lk(m);
+  cache.push_back({dev, kern, smem, (long)ncl});
   return ncl;
 }
 

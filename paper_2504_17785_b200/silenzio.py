@@ -51,7 +51,7 @@ def load():
         "silenzio_pbs_batch": ([V, V, V, U32, V, V, V, S, P, V, V], I),
         "silenzio_blind_rotate_batch": ([V, V, V, U32, V, V, S, P, V, V], I),
         "silenzio_blind_rotate_workspace_bytes": ([P, S], S),
-        "silenzio_pbs_batch_host": ([V, V, V, U32, V, V, V, S, S, P, V], I),
+        "silenzio_pbs_batch_host": ([V, V, V, U32, V, V, V, S, S, P, V, V], I),
         "silenzio_lwe_linear_batch": ([V, V, V, V, U32, U32, S, V, V], I),
         "silenzio_build_testpoly": ([V, U32, U32, U32, V, V], I),
         "silenzio_lwe_encrypt_batch": ([V, V, V, V, U32, S, V, V], I),
@@ -198,8 +198,25 @@ def keyswitch_batch(lwe_in, ksk, P, out=None, stream=None, tensor_cores=True, wo
     return out
 
 
+def _check_batch(lwe, in_words, lut_ids, luts, P, out, out_words):
+    """Shape / dtype checks the C ABI cannot make (it sees raw pointers)."""
+    count = lwe.shape[0]
+    if lwe.dtype != torch.int64 or lwe.dim() != 2 or lwe.shape[1] != in_words:
+        raise SilenzioError(f"ciphertexts must be int64 [count][{in_words}], got {lwe.dtype} {tuple(lwe.shape)}")
+    if lut_ids is not None and (lut_ids.dtype not in (torch.int32,) or lut_ids.numel() != count):
+        raise SilenzioError(f"lut_ids must be int32 (read as u32) with {count} entries, got {lut_ids.dtype} "
+                            f"{tuple(lut_ids.shape)}")
+    if luts.dtype != torch.int64 or luts.shape[-1] != P.N:
+        raise SilenzioError(f"luts must be int64 [num][{P.N}], got {luts.dtype} {tuple(luts.shape)}")
+    if out is not None and (out.dtype != torch.int64 or out.numel() != count * out_words):
+        raise SilenzioError(f"out must be int64 [{count}][{out_words}]")
+
+
 def pbs_batch(lwe_in, lut_ids, luts, fourier_bsk, ksk, P, out=None, workspace=None, stream=None):
     count = lwe_in.shape[0]
+    _check_batch(lwe_in, P.k * P.N + 1, lut_ids, luts, P, out, P.k * P.N + 1)
+    if workspace is not None and workspace.numel() * workspace.element_size() < pbs_workspace_bytes(P, count):
+        raise SilenzioError("workspace too small (silenzio_pbs_workspace_bytes)")
     if out is None:
         out = torch.empty((count, P.k * P.N + 1), dtype=torch.int64, device=lwe_in.device)
     if workspace is None:
@@ -217,6 +234,7 @@ def blind_rotate_workspace_bytes(P, count: int) -> int:
 
 def blind_rotate_batch(lwe_small, lut_ids, luts, fourier_bsk, P, out=None, workspace=None, stream=None):
     count = lwe_small.shape[0]
+    _check_batch(lwe_small, P.n + 1, lut_ids, luts, P, out, P.k * P.N + 1)
     if out is None:
         out = torch.empty((count, P.k * P.N + 1), dtype=torch.int64, device=lwe_small.device)
     if workspace is None:
@@ -229,13 +247,19 @@ def blind_rotate_batch(lwe_small, lut_ids, luts, fourier_bsk, P, out=None, works
     return out
 
 
-def pbs_batch_host(lwe_in_host, lut_ids_host, luts, fourier_bsk, ksk, P, out_host, workspace, chunk=0):
-    """Host-buffer PBS (chunked H2D / compute / D2H overlap inside the library)."""
+def pbs_batch_host(lwe_in_host, lut_ids_host, luts, fourier_bsk, ksk, P, out_host, workspace, chunk=0,
+                   stream=None):
+    """Host-buffer PBS (chunked H2D / compute / D2H overlap inside the library).
+    The library orders its copies after the work queued on `stream` (default:
+    torch's current stream, where luts / keys / workspace were produced)."""
     count = lwe_in_host.shape[0]
+    _check_batch(lwe_in_host, P.k * P.N + 1, lut_ids_host, luts, P, out_host, P.k * P.N + 1)
     num_luts = luts.shape[0] if luts.dim() == 2 else 1
+    if stream is None:
+        stream = torch.cuda.current_stream(luts.device)
     _check(load().silenzio_pbs_batch_host(_hptr(lwe_in_host), _hptr(lut_ids_host), _ptr(luts), num_luts,
                                           _ptr(fourier_bsk), _ptr(ksk), _hptr(out_host), count, chunk,
-                                          ctypes.byref(make_params(P)), _ptr(workspace)))
+                                          ctypes.byref(make_params(P)), _ptr(workspace), _stream(stream)))
     return out_host
 
 

@@ -97,3 +97,32 @@ def test_maximum_count_is_rejected_before_any_launch(lib):
                                 None) == -5
     assert L.silenzio_blind_rotate_batch(fake, None, fake, 1, fake, ctypes.c_void_p(512), n, ctypes.byref(P), None,
                                          None) == -5
+
+
+def test_binding_rejects_malformed_tensors_before_the_call():
+    """silenzio.py checks what the C ABI cannot see through raw pointers: an
+    int64 lut_ids tensor (would be read as u32 pairs), ciphertext widths other
+    than k*N+1 (n+1 for the blind rotation), LUT widths other than N, and a
+    wrong-sized out tensor. No GPU: the checks run first."""
+    import pytest
+    import torch
+    from paper_2504_17785_b200 import silenzio
+    from synth import get_params
+    P = get_params("A_SMALLN")
+    ct = torch.zeros((3, P.big_dim + 1), dtype=torch.int64)
+    luts = torch.zeros((1, P.N), dtype=torch.int64)
+    ok_ids = torch.zeros(3, dtype=torch.int32)
+    bad = [
+        dict(lwe_in=ct, lut_ids=torch.zeros(3, dtype=torch.int64), luts=luts),
+        dict(lwe_in=ct, lut_ids=torch.zeros(2, dtype=torch.int32), luts=luts),
+        dict(lwe_in=ct[:, :-1].contiguous(), lut_ids=ok_ids, luts=luts),
+        dict(lwe_in=ct, lut_ids=ok_ids, luts=luts[:, :-1].contiguous()),
+        dict(lwe_in=ct.to(torch.int32), lut_ids=ok_ids, luts=luts),
+    ]
+    for kw in bad:
+        with pytest.raises(silenzio.SilenzioError):
+            silenzio.pbs_batch(kw["lwe_in"], kw["lut_ids"], kw["luts"], None, None, P)
+    with pytest.raises(silenzio.SilenzioError):
+        silenzio.pbs_batch(ct, ok_ids, luts, None, None, P, out=torch.zeros((2, P.big_dim + 1), dtype=torch.int64))
+    with pytest.raises(silenzio.SilenzioError):
+        silenzio.blind_rotate_batch(ct, ok_ids, luts, None, P)   # expects n+1 words
