@@ -339,6 +339,12 @@ int silenzio_pbs_trace_begin(int kind, uint64_t *records, size_t max_records, ui
                              size_t in_words, size_t out_words, size_t lut_words);
 long silenzio_pbs_trace_end(int kind, uint64_t *elements_seen);
 
+/* Debug builds only (-DSZ_FFT_MARGIN=1, tools/fft_margin.py): the largest
+ * |x - round(x)| and |x| over every limb value the set-A blind rotations
+ * rounded since the last call (R20: exact while < 1/2 and < 2^51);
+ * resets both. Release builds return SILENZIO_ERR_UNSUPPORTED. */
+int silenzio_debug_fft_margin(double *max_frac, double *max_abs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "nvtx.cuh"
 
 namespace sz {
 int launch_blind_rotate(const u64 *, const u32 *, const u64 *, u32, const void *, u64 *, size_t,
@@ -143,6 +144,7 @@ static int run_keyswitch(const u64 *in, const u64 *ksk, u64 *out, size_t count, 
 }
 
 int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fbsk, const silenzio_params *P, void *stream) {
+  SZ_RANGE("bsk_to_fourier");
   int st = check_params(P);
   if (st) return st;
   if (!bsk || !fbsk) return SILENZIO_ERR_NULL_POINTER;
@@ -155,6 +157,7 @@ int silenzio_bsk_to_fourier(const uint64_t *bsk, void *fbsk, const silenzio_para
 
 int silenzio_keyswitch_batch(const uint64_t *in, const uint64_t *ksk, uint64_t *out, size_t count,
                              const silenzio_params *P, void *workspace, void *stream) {
+  SZ_RANGE("keyswitch_batch");
   int st = check_params(P);
   if (st) return st;
   if ((st = check_ks_params(P))) return st;
@@ -168,6 +171,7 @@ int silenzio_keyswitch_batch(const uint64_t *in, const uint64_t *ksk, uint64_t *
 int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_ids, const uint64_t *luts,
                                 uint32_t num_luts, const void *fbsk, uint64_t *out, size_t count,
                                 const silenzio_params *P, void *workspace, void *stream) {
+  SZ_RANGE("blind_rotate_batch");
   int st = check_params(P);
   if (st) return st;
   if ((st = check_br_supported(P))) return st;
@@ -189,6 +193,7 @@ int silenzio_blind_rotate_batch(const uint64_t *lwe_small, const uint32_t *lut_i
 int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64_t *luts, uint32_t num_luts,
                        const void *fbsk, const uint64_t *ksk, uint64_t *out, size_t count,
                        const silenzio_params *P, void *workspace, void *stream) {
+  SZ_RANGE("pbs_batch");
   int st = check_params(P);
   if (st) return st;
   if ((st = check_ks_params(P))) return st;
@@ -206,7 +211,10 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
   u64 *small = reinterpret_cast<u64 *>(workspace);
   unsigned char *br_ws = reinterpret_cast<unsigned char *>(workspace) + round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256);
   unsigned char *ks_ws = br_ws + silenzio_blind_rotate_workspace_bytes(P, count);
-  if ((st = run_keyswitch(in, ksk, small, count, P, ks_ws, sz_stream(stream)))) return st;
+  {
+    SZ_RANGE("pbs.keyswitch");
+    if ((st = run_keyswitch(in, ksk, small, count, P, ks_ws, sz_stream(stream)))) return st;
+  }
   return silenzio_blind_rotate_batch(small, lut_ids, luts, num_luts, fbsk, out, count, P, br_ws, stream);
 }
 
@@ -239,6 +247,7 @@ size_t silenzio_pbs_host_workspace_bytes(const silenzio_params *P, size_t chunk)
 int silenzio_pbs_batch_host(const uint64_t *in_h, const uint32_t *ids_h, const uint64_t *luts, uint32_t num_luts,
                             const void *fbsk, const uint64_t *ksk, uint64_t *out_h, size_t count, size_t chunk,
                             const silenzio_params *P, void *workspace, void *stream) {
+  SZ_RANGE("pbs_batch_host");
   int st = check_params(P);
   if (st) return st;
   if (count == 0) return SILENZIO_OK;
@@ -298,6 +307,7 @@ int silenzio_pbs_batch_host(const uint64_t *in_h, const uint32_t *ids_h, const u
 
 int silenzio_lwe_linear_batch(const uint64_t *in, const uint32_t *idx, const int64_t *coef, const uint64_t *cst,
                               uint32_t terms, uint32_t dim, size_t count, uint64_t *out, void *stream) {
+  SZ_RANGE("lwe_linear_batch");
   if (count == 0) return SILENZIO_OK;
   if (!in || !idx || !coef || !out) return SILENZIO_ERR_NULL_POINTER;
   if (terms == 0 || dim == 0) return SILENZIO_ERR_INVALID_PARAM;

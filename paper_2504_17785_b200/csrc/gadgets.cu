@@ -18,6 +18,7 @@
 //                       tree of T3 reductions.
 
 #include "gadget_util.cuh"
+#include "nvtx.cuh"
 
 namespace szg {
 
@@ -126,6 +127,7 @@ size_t silenzio_rns_matmul_workspace_bytes(const silenzio_params *P, uint32_t a,
 int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32_t b, uint32_t c,
                         const uint32_t *moduli, uint32_t k, uint64_t *out, const void *fbsk, const uint64_t *ksk,
                         const silenzio_params *P, void *workspace, size_t workspace_bytes, void *stream) {
+  SZ_RANGE("rns_matmul");
   if (!X || !W || !moduli || !out || !fbsk || !ksk || !P) return SILENZIO_ERR_NULL_POINTER;
   if (!workspace) return SILENZIO_ERR_WORKSPACE;
   if (a == 0 || b == 0 || c == 0 || k == 0) return SILENZIO_ERR_COUNT;

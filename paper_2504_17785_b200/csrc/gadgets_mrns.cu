@@ -6,6 +6,7 @@
 // Thin drivers: they sequence linear LWE ops and PBS calls; every ciphertext
 // operation runs in a kernel. Schedule: DESIGN.md §Config 4.
 #include "gadget_util.cuh"
+#include "nvtx.cuh"
 
 using namespace szg;
 
@@ -119,6 +120,7 @@ size_t silenzio_gadget_workspace_bytes(const silenzio_params *P, uint32_t k, siz
 int silenzio_rns2mrns(const uint64_t *in, const uint32_t *moduli_host, uint32_t k, size_t count, uint64_t *out,
                       const void *fbsk, const uint64_t *ksk, const silenzio_params *P, void *workspace,
                       size_t workspace_bytes, void *stream) {
+  SZ_RANGE("rns2mrns");
   if (!in || !moduli_host || !out || !fbsk || !ksk || !P) return SILENZIO_ERR_NULL_POINTER;
   if (!workspace || workspace_bytes < silenzio_gadget_workspace_bytes(P, k, count)) return SILENZIO_ERR_WORKSPACE;
   if (P->poly_size != 2048 || k < 1) return SILENZIO_ERR_UNSUPPORTED;
@@ -141,6 +143,7 @@ int silenzio_rns2mrns(const uint64_t *in, const uint32_t *moduli_host, uint32_t 
 int silenzio_rns_sign_abs(const uint64_t *in, const uint32_t *moduli_host, uint32_t k, size_t count,
                           uint64_t *sign_out, uint64_t *abs_out, const void *fbsk, const uint64_t *ksk,
                           const silenzio_params *P, void *workspace, size_t workspace_bytes, void *stream) {
+  SZ_RANGE("rns_sign_abs");
   if (!in || !moduli_host || !sign_out || !abs_out || !fbsk || !ksk || !P) return SILENZIO_ERR_NULL_POINTER;
   if (!workspace || workspace_bytes < silenzio_gadget_workspace_bytes(P, k, count)) return SILENZIO_ERR_WORKSPACE;
   if (P->poly_size != 2048 || k < 1) return SILENZIO_ERR_UNSUPPORTED;
@@ -186,6 +189,7 @@ int silenzio_rns_sign_abs(const uint64_t *in, const uint32_t *moduli_host, uint3
 int silenzio_mrns_bitlen_max(const uint64_t *digits, uint32_t k, size_t count, uint64_t *bitlen_out,
                              uint64_t *max_out, const void *fbsk, const uint64_t *ksk, const silenzio_params *P,
                              void *workspace, size_t workspace_bytes, void *stream) {
+  SZ_RANGE("mrns_bitlen_max");
   if (!digits || !bitlen_out || !max_out || !fbsk || !ksk || !P) return SILENZIO_ERR_NULL_POINTER;
   if (!workspace || workspace_bytes < silenzio_gadget_workspace_bytes(P, k, count)) return SILENZIO_ERR_WORKSPACE;
   if (P->poly_size != 2048) return SILENZIO_ERR_UNSUPPORTED;
@@ -236,6 +240,7 @@ int silenzio_mrns_bitlen_max(const uint64_t *digits, uint32_t k, size_t count, u
 int silenzio_int_ce_grad(const uint64_t *Yhat, const uint64_t *Y, uint32_t a, uint32_t b, uint64_t *out,
                          const void *fbsk, const uint64_t *ksk, const silenzio_params *P, void *workspace,
                          size_t workspace_bytes, void *stream) {
+  SZ_RANGE("int_ce_grad");
   if (!Yhat || !Y || !out || !fbsk || !ksk || !P) return SILENZIO_ERR_NULL_POINTER;
   const size_t count = (size_t)a * b;
   if (!workspace || workspace_bytes < silenzio_gadget_workspace_bytes(P, 1, count)) return SILENZIO_ERR_WORKSPACE;
@@ -398,6 +403,7 @@ int silenzio_mrns_digit_combine(const uint64_t *top_digit, const uint64_t *abs_d
                                 const silenzio_params *pa, const void *fbsk_b, const silenzio_params *pb,
                                 const uint64_t *ksk_ab, const silenzio_params *pab, const uint64_t *ksk_ba,
                                 const silenzio_params *pba, void *workspace, size_t workspace_bytes, void *stream) {
+  SZ_RANGE("mrns_digit_combine");
   if (!top_digit || !abs_digits || !maxes || !out || !maxbit_out || !fbsk_a || !ksk_a || !pa || !fbsk_b || !pb ||
       !ksk_ab || !pab || !ksk_ba || !pba)
     return SILENZIO_ERR_NULL_POINTER;

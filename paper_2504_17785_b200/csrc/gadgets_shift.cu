@@ -12,6 +12,7 @@
 #include <thread>
 
 #include "common.cuh"
+#include "nvtx.cuh"
 
 extern "C" {
 size_t silenzio_gadget_workspace_bytes(const silenzio_params *, uint32_t, size_t);
@@ -53,6 +54,7 @@ int silenzio_shift2msbs_pm(const uint64_t *residues, const uint32_t *moduli_host
                            const silenzio_params *pb, const uint64_t *ksk_ab, const silenzio_params *pab,
                            const uint64_t *ksk_ba, const silenzio_params *pba, void *workspace,
                            size_t workspace_bytes, void *stream) {
+  SZ_RANGE("shift2msbs_pm");
   if (!residues || !moduli_host || !out || !maxbit_out || !fbsk_a || !ksk_a || !pa || !fbsk_b || !pb || !ksk_ab ||
       !pab || !ksk_ba || !pba)
     return SILENZIO_ERR_NULL_POINTER;

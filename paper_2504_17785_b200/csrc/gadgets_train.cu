@@ -9,6 +9,7 @@
 //   silenzio_relu_mask      error sign times the ReLU_x derivative (R25)
 //   silenzio_weight_update  clip(W - G) for G in {-1, 0, 1} (Alg. 6 last line, R23)
 #include "gadget_util.cuh"
+#include "nvtx.cuh"
 
 extern "C" int silenzio_rns2mrns(const uint64_t *, const uint32_t *, uint32_t, size_t, uint64_t *, const void *,
                                  const uint64_t *, const silenzio_params *, void *, size_t, void *);
@@ -54,6 +55,7 @@ size_t silenzio_train_workspace_bytes(const silenzio_params *P, uint32_t k, size
 
 int silenzio_channel16(const uint64_t *in, size_t count, uint64_t *out, const void *fbsk, const uint64_t *ksk,
                        const silenzio_params *P, void *workspace, size_t workspace_bytes, void *stream) {
+  SZ_RANGE("channel16");
   int rc = check_common(in, out, fbsk, ksk, P, workspace, workspace_bytes, silenzio_train_workspace_bytes(P, 1, count));
   if (rc) return rc;
   if (count == 0) return SILENZIO_OK;
@@ -78,6 +80,7 @@ int silenzio_channel16(const uint64_t *in, size_t count, uint64_t *out, const vo
 int silenzio_rns_sign3(const uint64_t *residues, const uint32_t *moduli_host, uint32_t k, size_t count,
                        uint64_t *out, const void *fbsk, const uint64_t *ksk, const silenzio_params *P,
                        void *workspace, size_t workspace_bytes, void *stream) {
+  SZ_RANGE("rns_sign3");
   int rc = check_common(residues, out, fbsk, ksk, P, workspace, workspace_bytes,
                         silenzio_train_workspace_bytes(P, k, count));
   if (rc) return rc;
@@ -118,6 +121,7 @@ int silenzio_rns_sign3(const uint64_t *residues, const uint32_t *moduli_host, ui
 int silenzio_relu_cap(const uint64_t *in, size_t count, int32_t cap, uint64_t *out, const void *fbsk,
                       const uint64_t *ksk, const silenzio_params *P, void *workspace, size_t workspace_bytes,
                       void *stream) {
+  SZ_RANGE("relu_cap");
   int rc = check_common(in, out, fbsk, ksk, P, workspace, workspace_bytes, silenzio_train_workspace_bytes(P, 1, count));
   if (rc) return rc;
   if (cap < 0 || cap > 7) return SILENZIO_ERR_WINDOW;
@@ -132,6 +136,7 @@ int silenzio_relu_cap(const uint64_t *in, size_t count, int32_t cap, uint64_t *o
 int silenzio_relu_mask(const uint64_t *e, const uint64_t *s, size_t count, int32_t cap, uint64_t *out,
                        const void *fbsk, const uint64_t *ksk, const silenzio_params *P, void *workspace,
                        size_t workspace_bytes, void *stream) {
+  SZ_RANGE("relu_mask");
   int rc = check_common(e, s, fbsk, ksk, P, workspace, workspace_bytes, silenzio_train_workspace_bytes(P, 1, count));
   if (rc) return rc;
   if (!out) return SILENZIO_ERR_NULL_POINTER;
@@ -155,6 +160,7 @@ int silenzio_relu_mask(const uint64_t *e, const uint64_t *s, size_t count, int32
 int silenzio_weight_update(const uint64_t *w, const uint64_t *g, size_t count, int32_t wmin, int32_t wmax,
                            uint64_t *out, const void *fbsk, const uint64_t *ksk, const silenzio_params *P,
                            void *workspace, size_t workspace_bytes, void *stream) {
+  SZ_RANGE("weight_update");
   int rc = check_common(w, g, fbsk, ksk, P, workspace, workspace_bytes, silenzio_train_workspace_bytes(P, 1, count));
   if (rc) return rc;
   if (!out) return SILENZIO_ERR_NULL_POINTER;

@@ -24,6 +24,7 @@
 // Fourier BSK layout for this kernel: [n][P][2 (o)][2 (row)][32 (r)][32 (lane)]
 // where (r, lane) holds the spectrum at index lane + 32 r, times 1/M.
 #include <cmath>
+#include <cstring>
 #include <mutex>
 
 #include "fft.cuh"
@@ -157,12 +158,39 @@ __device__ __forceinline__ double2 untwist_unscaled(double2 a) {
 
 // inverse untwist of output m fused with the exact rounding of the limb:
 // bits(s_m * u + 1.5 * 2^52) = round(x conj(w^{32m})) + bits(1.5 * 2^52), |.| < 2^51
+#ifndef SZ_FFT_MARGIN
+#define SZ_FFT_MARGIN 0  // 1: debug build recording the rounding margin of every limb (tools/fft_margin.py)
+#endif
+#if SZ_FFT_MARGIN
+// max |x - round(x)| (as f64 bits: non-negative doubles order like u64) and max |x|
+// over every rounded limb value of the launch (R20: exactness needs
+// |error| < 1/2 and |x| < 2^51)
+__device__ unsigned long long g_margin_frac, g_margin_abs;
+__device__ __forceinline__ void margin_note(double x, u64 bits) {
+  const double r = __longlong_as_double((long long)bits) - 6755399441055744.0;  // round(x), exact
+  unsigned long long f = (unsigned long long)__double_as_longlong(fabs(x - r));
+  unsigned long long a = (unsigned long long)__double_as_longlong(fabs(x));
+  // warp-level max first (one atomic per warp)
+  for (int d = 16; d; d >>= 1) {
+    f = max(f, (unsigned long long)__shfl_xor_sync(0xffffffffu, f, d));
+    a = max(a, (unsigned long long)__shfl_xor_sync(0xffffffffu, a, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&g_margin_frac, f);
+    atomicMax(&g_margin_abs, a);
+  }
+}
+#endif
 template <int M>
 __device__ __forceinline__ void untwist_round_t(double2 y, u64 &bx, u64 &by) {
   const double2 u = untwist_unscaled<M>(y);
   constexpr double s = twist_scale(M);
   bx = (u64)__double_as_longlong(fma(u.x, s, 6755399441055744.0));
   by = (u64)__double_as_longlong(fma(u.y, s, 6755399441055744.0));
+#if SZ_FFT_MARGIN
+  margin_note(u.x * s, bx);
+  margin_note(u.y * s, by);
+#endif
 }
 __device__ __forceinline__ void untwist_round(double2 y, int m, u64 &bx, u64 &by) {
   switch (m & 31) {
@@ -554,6 +582,174 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   if (wid == 0) tmem_dealloc(tmem_slot, kTmemCols);
 }
 
+// ------------------------------------------------- latency kernel (small batches)
+// One ciphertext per CTA (8 warps), for batches too small to fill the GPU with
+// four ciphertexts per SM: the per-PBS latency, not the FP64 throughput, is
+// what such a launch waits for. Same transform, tables,
+// Fourier-BSK layout and arithmetic as blind_rotate_warp_kernel; the eight
+// FFTs of a CMux are spread over the warps instead of two:
+//   phase F  warps 0, 1 (GLWE component r = warp): ACC_r += the three limb
+//            contributions of the previous CMux, digits of X^a ACC_r - ACC_r,
+//            forward FFT, D^_r to shared memory;
+//   phase I  warps 2..7, one per (output o, limb p): MAC of D^_0, D^_1 with
+//            BSK_i[p][o] (prefetched into registers during phase F), inverse
+//            FFT with the fused untwist + exact rounding, the limb's shifted
+//            contribution written to the warp's own buffer.
+// Two CTA barriers per CMux separate the phases.
+constexpr int kLatThreads = 256;
+__host__ __device__ constexpr size_t lat_smem_bytes(int n) {
+  return 8 * (size_t)kXbuf * sizeof(double2)   // per-warp FFT buffers (inverse warps: + contributions)
+         + 2 * (size_t)kM * sizeof(double2)    // D^_0, D^_1 in slot order
+         + 2 * (size_t)kM * sizeof(ulonglong2) // ACC_0, ACC_1 as coefficient pairs (s, s + 1024)
+         + abar_bytes(n);
+}
+
+// phase F of one CMux for GLWE component r (warps 0, 1)
+template <int P>
+__device__ __forceinline__ void lat_forward(ulonglong2 *ac, const ulonglong2 *contrib, double2 *dhat_r,
+                                            double2 *xbuf, int a, bool add, int lane, u64 half_q, int blog) {
+  if (add) {  // ACC_r += the limb contributions of the previous CMux
+#pragma unroll 4
+    for (int s = lane; s < kM; s += 32) {
+      ulonglong2 v = ac[s];
+#pragma unroll
+      for (int q = 0; q < P; q++) {
+        const ulonglong2 cq = contrib[q * kXbuf + s];
+        v.x += cq.x;
+        v.y += cq.y;
+      }
+      ac[s] = v;
+    }
+    __syncwarp();
+  }
+  // digits of X^a ACC_r - ACC_r (a4.1-a4.2), as in blind_rotate_warp_kernel
+  double2 x[32];
+#pragma unroll
+  for (int m = 0; m < 32; m++) {
+    const int src0 = (lane + 32 * m - a) & (2 * kN - 1);
+    const int qd = src0 >> 10;
+    const ulonglong2 pr = ac[src0 & 1023];
+    const ulonglong2 own = ac[lane + 32 * m];
+    u64 r0 = (qd & 1) ? pr.y : pr.x, r1 = (qd & 1) ? pr.x : pr.y;
+    if (qd >= 2) r0 = (u64)0 - r0;
+    if (qd == 1 || qd == 2) r1 = (u64)0 - r1;
+    x[m] = make_double2((double)((i64)(r0 - own.x + half_q) >> (64 - blog)),
+                        (double)((i64)(r1 - own.y + half_q) >> (64 - blog)));
+  }
+  fwd_fft32(x, xbuf, lane);
+#pragma unroll
+  for (int k2 = 0; k2 < 32; k2++) dhat_r[32 * k2 + lane] = x[k2];
+}
+
+template <int P>
+__global__ void __launch_bounds__(kLatThreads, 1) blind_rotate_lat_kernel(Args A) {
+  static_assert(P >= 1 && P <= 3, "1..3 limbs");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int n = A.n, w = A.w, blog = A.base_log;
+  double2 *xbuf_all = reinterpret_cast<double2 *>(smem);
+  double2 *dhat = xbuf_all + 8 * kXbuf;                                  // [2][32 k2][32 lane]
+  ulonglong2 *accp = reinterpret_cast<ulonglong2 *>(dhat + 2 * kM);      // [2][1024]
+  unsigned short *abar = reinterpret_cast<unsigned short *>(accp + 2 * kM);
+  const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
+  double2 *xbuf = xbuf_all + wid * kXbuf;
+  const u64 half_q = 1ull << (63 - blog);
+  for (long c = blockIdx.x; c < A.count; c += gridDim.x) {
+    const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
+    for (int i = tid; i < n; i += kLatThreads) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2N);
+    if (wid < 2) {
+      // ---------------- forward warps: component r = wid
+      const int r = wid;
+      ulonglong2 *ac = accp + r * kM;
+      const ulonglong2 *contrib = reinterpret_cast<const ulonglong2 *>(xbuf_all + (2 + 3 * r) * kXbuf);
+      {  // ACC init (a3): ACC = (0, X^{-b~} v) as pairs (s, s + 1024)
+        const int bt = (int)sz_modswitch(lwe[n], kLog2_2N);
+        u32 id = A.lut_ids ? A.lut_ids[c] : 0u;
+        if (id >= A.num_luts) id = 0;
+        const u64 *v = A.luts + (size_t)id * kN;
+        for (int s = lane; s < kM; s += 32)
+          ac[s] = make_ulonglong2(acc_init(v, s, bt, r), acc_init(v, s + 1024, bt, r));
+      }
+      __syncthreads();  // abar complete
+      for (int i = 0; i < n; i++) {
+        lat_forward<P>(ac, contrib, dhat + r * kM, xbuf, abar[i], i > 0, lane, half_q, blog);
+        __syncthreads();  // D^ published (and the previous contributions consumed)
+        __syncthreads();  // contributions of CMux i written
+      }
+      // ACC += the last contributions, then sample extraction (a5)
+      u64 *out = A.lwe_out + (size_t)c * (kN + 1);
+      for (int s = lane; s < kM; s += 32) {
+        ulonglong2 v = ac[s];
+#pragma unroll
+        for (int q = 0; q < P; q++) {
+          const ulonglong2 cq = contrib[q * kXbuf + s];
+          v.x += cq.x;
+          v.y += cq.y;
+        }
+        if (r == 0) {  // a'[0] = A[0], a'[j] = -A[N - j]
+          if (s == 0) out[0] = v.x;
+          else out[kN - s] = (u64)0 - v.x;
+          out[kN - (s + 1024)] = (u64)0 - v.y;
+        } else if (s == 0) {
+          out[kN] = v.x;  // b' = B[0]
+        }
+      }
+    } else {
+      // ---------------- inverse warps: warp 2 + 3 o + (P - 1 - p) (warps past 2 + 3 o + P - 1 idle)
+      const int job = wid - 2, o = job / 3, p = P - 1 - job % 3;
+      const bool active = job % 3 < P;
+      const u64 limb_off =
+          kMagicBits + (P >= 2 ? (kMagicBits << w) : 0ull) + (P >= 3 ? (kMagicBits << (2 * w)) : 0ull);
+      double2 g0[32], g1[32];  // BSK_i[p][o] rows 0 and 1 at slots lane + 32 k2
+      auto load_g = [&](int i) {
+        const double2 *G = A.fbsk + (((size_t)i * P + p) * 2 + o) * 2 * kM + lane;
+#pragma unroll
+        for (int k2 = 0; k2 < 32; k2++) {
+          g0[k2] = __ldg(G + 32 * k2);
+          g1[k2] = __ldg(G + kM + 32 * k2);
+        }
+      };
+      if (active) load_g(0);
+      __syncthreads();  // abar complete
+      for (int i = 0; i < n; i++) {
+        __syncthreads();  // D^ published
+        if (active) {
+          double2 (&y)[32] = g0;  // the MAC output overwrites the BSK row-0 registers
+#pragma unroll
+          for (int k2 = 0; k2 < 32; k2++) {
+            double2 acc = make_double2(0.0, 0.0);
+            cmac(acc, dhat[32 * k2 + lane], g0[k2]);
+            cmac(acc, dhat[kM + 32 * k2 + lane], g1[k2]);
+            y[k2] = acc;
+          }
+          ulonglong2 *contrib = reinterpret_cast<ulonglong2 *>(xbuf);
+          if constexpr (P == 3) {
+            inv_fft32<false>(y, xbuf, lane);
+            __syncwarp();  // the transposition's readers of xbuf are done
+            const u64 off = (p == 0) ? limb_off : 0ull;  // all limbs' magic share, removed once
+#pragma unroll
+            for (int m = 0; m < 32; m++) {
+              u64 bx, by;
+              untwist_round(y[m], m, bx, by);
+              contrib[lane + 32 * m] = make_ulonglong2((bx << (p * w)) - off, (by << (p * w)) - off);
+            }
+          } else {
+            inv_fft32<true>(y, xbuf, lane);
+            __syncwarp();
+#pragma unroll
+            for (int m = 0; m < 32; m++)
+              contrib[lane + 32 * m] =
+                  make_ulonglong2(limb_to_torus(y[m].x, p, P, w), limb_to_torus(y[m].y, p, P, w));
+          }
+          // the next BSK slice: its loads land while phase F of CMux i + 1 runs
+          if (i + 1 < n) load_g(i + 1);
+        }
+        __syncthreads();  // contributions written
+      }
+    }
+    __syncthreads();  // abar / ACC / contributions reuse by the next ciphertext
+  }
+}
+
 // --------------------------------------------------------- BSK -> Fourier
 struct B2FArgs {
   const u64 *bsk;  // [n][2 (rows)][2 (o)][N]
@@ -603,6 +799,35 @@ long blind_rotate_warp_wave() {
 
 long blind_rotate_warp_launches(size_t count) { return count ? 1 : 0; }
 
+// SZ_FFT_MARGIN debug builds: read-and-reset the recorded rounding margin
+extern "C" int silenzio_debug_fft_margin(double *max_frac, double *max_abs) {
+#if SZ_FFT_MARGIN
+  unsigned long long f = 0, a = 0, z = 0;
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(&f, w32::g_margin_frac, 8));
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(&a, w32::g_margin_abs, 8));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_frac, &z, 8));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_abs, &z, 8));
+  double df, da;
+  memcpy(&df, &f, 8);
+  memcpy(&da, &a, 8);
+  if (max_frac) *max_frac = df;
+  if (max_abs) *max_abs = da;
+  return SILENZIO_OK;
+#else
+  (void)max_frac;
+  (void)max_abs;
+  return SILENZIO_ERR_UNSUPPORTED;
+#endif
+}
+
+// Largest batch the latency kernel takes (one ciphertext per SM per wave):
+// up to SZ_LAT_WAVES waves of it beat one launch of the four-ciphertext kernel
+// (measured). SZ_LAT_WAVES = 0 disables it.
+#ifndef SZ_LAT_WAVES
+#define SZ_LAT_WAVES 3
+#endif
+long blind_rotate_lat_max(long sms) { return SZ_LAT_WAVES * sms; }
+
 int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
                              const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
                              cudaStream_t stream) {
@@ -624,10 +849,24 @@ int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64
   A.n = (int)P->lwe_dim;
   A.base_log = (int)P->pbs_base_log;
   A.w = (int)P->limb_bits;
-  const size_t smem = w32::smem_bytes(A.n);
-  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const long wave = blind_rotate_warp_wave();
   if (wave <= 0) return SILENZIO_ERR_CUDA;
+  const long sms = wave / w32::kCts;
+  if ((long)count <= blind_rotate_lat_max(sms) && w32::lat_smem_bytes(A.n) <= 227 * 1024) {
+    // small batch: one ciphertext per CTA, the eight FFTs of a CMux on eight warps
+    void (*lk)(w32::Args) = nullptr;
+    if (P->fft_limbs == 1) lk = w32::blind_rotate_lat_kernel<1>;
+    if (P->fft_limbs == 2) lk = w32::blind_rotate_lat_kernel<2>;
+    if (P->fft_limbs == 3) lk = w32::blind_rotate_lat_kernel<3>;
+    const size_t lsmem = w32::lat_smem_bytes(A.n);
+    SZ_CUDA_OK(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
+    const long grid = (long)count < sms ? (long)count : sms;
+    lk<<<(unsigned)grid, w32::kLatThreads, lsmem, stream>>>(A);
+    SZ_LAUNCH_OK();
+    return SILENZIO_OK;
+  }
+  const size_t smem = w32::smem_bytes(A.n);
+  SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // one persistent launch, CTA b handles groups b, b + grid, ... (grid-stride).
   // CTAs drift apart in i over a long batch, but the bulk-copy stage prefetch
   // tolerates the resulting L2 misses: measured +3.8 % at 131 072 ciphertexts

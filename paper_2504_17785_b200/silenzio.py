@@ -78,6 +78,7 @@ def load():
         "silenzio_weight_update": ([V, V, S, ctypes.c_int32, ctypes.c_int32, V, V, V, P, V, S, V], I),
         "silenzio_pbs_trace_begin": ([I, V, S, ctypes.c_uint64, ctypes.c_uint64, S, S, S], I),
         "silenzio_pbs_trace_end": ([I, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_long),
+        "silenzio_debug_fft_margin": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -101,6 +102,7 @@ def exported_symbols():
         "silenzio_shift2msbs_workspace_bytes", "silenzio_shift2msbs_pm",
         "silenzio_train_workspace_bytes", "silenzio_channel16", "silenzio_rns_sign3", "silenzio_relu_cap",
         "silenzio_relu_mask", "silenzio_weight_update", "silenzio_pbs_trace_begin", "silenzio_pbs_trace_end",
+        "silenzio_debug_fft_margin",
     ]
 
 
@@ -521,3 +523,11 @@ class PbsTrace:
         r = self.records.cpu().numpy().view(np.uint64)
         a, b, c = self.words
         return r[:, :a], r[:, a:a + b], r[:, a + b:a + b + c], r[:, -2].astype(np.int64), r[:, -1].astype(np.int64)
+
+
+def debug_fft_margin():
+    """(max |x - round(x)|, max |x|) over the limbs rounded since the last call
+    (debug builds with -DSZ_FFT_MARGIN=1 only)."""
+    f, a = ctypes.c_double(0), ctypes.c_double(0)
+    _check(load().silenzio_debug_fft_margin(ctypes.byref(f), ctypes.byref(a)))
+    return f.value, a.value
