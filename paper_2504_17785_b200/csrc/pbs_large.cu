@@ -23,13 +23,6 @@
 
 namespace sz {
 
-// pbs_cluster2.cu: two ciphertexts per R-CTA cluster (sets C and B at level 2)
-bool blind_rotate_cluster2_supported(const silenzio_params *P);
-int launch_blind_rotate_cluster2(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
-                                 const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
-                                 cudaStream_t stream);
-int launch_bsk_to_fourier_cluster2(const u64 *bsk, void *fbsk, const silenzio_params *P, cudaStream_t stream);
-
 __constant__ double2 c_twistL[16];  // e^{i pi m / 32}: w^{256 m} for N = 8192 (same values as N = 2048)
 
 constexpr int kNL = 8192;
@@ -402,7 +395,6 @@ __global__ void __launch_bounds__(256) bsk_to_fourier_large_kernel(B2FLArgs A) {
 }
 
 long blind_rotate_large_wave(const silenzio_params *P) {
-  if (blind_rotate_cluster2_supported(P)) return 1L << 40;  // one persistent launch for any count
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return -1;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
@@ -413,8 +405,6 @@ long blind_rotate_large_wave(const silenzio_params *P) {
 int launch_blind_rotate_large(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
                               const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
                               cudaStream_t stream) {
-  if (blind_rotate_cluster2_supported(P))
-    return launch_blind_rotate_cluster2(lwe_small, lut_ids, luts, num_luts, fbsk, lwe_out, count, P, stream);
   int st = ensure_tables_large();
   if (st) return st;
   BRLArgs A;
@@ -453,7 +443,6 @@ int launch_blind_rotate_large(const u64 *lwe_small, const u32 *lut_ids, const u6
 }
 
 int launch_bsk_to_fourier_large(const u64 *bsk, void *fbsk, const silenzio_params *P, cudaStream_t stream) {
-  if (blind_rotate_cluster2_supported(P)) return launch_bsk_to_fourier_cluster2(bsk, fbsk, P, stream);
   int st = ensure_tables_large();
   if (st) return st;
   B2FLArgs A;
@@ -1086,22 +1075,19 @@ static long cluster_grid(const silenzio_params *P, void (*kern)(BRHArgs), size_t
 }
 
 size_t blind_rotate_huge_ws_bytes(const silenzio_params *P, size_t count) {
-  if (blind_rotate_cluster2_supported(P)) return 0;
   const long cap = huge_inflight();
   const long inflight = (long)count < cap ? (long)count : cap;
   return (size_t)inflight * brh_ws_per_ct(2 * (int)P->pbs_level);
 }
 
 long blind_rotate_huge_wave(const silenzio_params *P) {
-  if (blind_rotate_cluster2_supported(P) || cluster_path(P)) return 1L << 40;  // one persistent launch for any count
+  if (cluster_path(P)) return 1L << 40;  // one persistent launch for any count
   return huge_inflight();
 }
 
 int launch_blind_rotate_huge(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
                              const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
                              void *workspace, cudaStream_t stream) {
-  if (blind_rotate_cluster2_supported(P))
-    return launch_blind_rotate_cluster2(lwe_small, lut_ids, luts, num_luts, fbsk, lwe_out, count, P, stream);
   int st = ensure_tables_huge();
   if (st) return st;
   BRHArgs A;
@@ -1151,7 +1137,6 @@ int launch_blind_rotate_huge(const u64 *lwe_small, const u32 *lut_ids, const u64
 }
 
 int launch_bsk_to_fourier_huge(const u64 *bsk, void *fbsk, const silenzio_params *P, cudaStream_t stream) {
-  if (blind_rotate_cluster2_supported(P)) return launch_bsk_to_fourier_cluster2(bsk, fbsk, P, stream);
   int st = ensure_tables_huge();
   if (st) return st;
   B2FHArgs A;

@@ -217,7 +217,7 @@ def _check_batch(lwe, in_words, lut_ids, luts, P, out, out_words):
 def pbs_batch(lwe_in, lut_ids, luts, fourier_bsk, ksk, P, out=None, workspace=None, stream=None):
     count = lwe_in.shape[0]
     _check_batch(lwe_in, P.k * P.N + 1, lut_ids, luts, P, out, P.k * P.N + 1)
-    if workspace is not None and workspace.numel() * workspace.element_size() < pbs_workspace_bytes(P, count):
+    if count and workspace is not None and workspace.numel() * workspace.element_size() < pbs_workspace_bytes(P, count):
         raise SilenzioError("workspace too small (silenzio_pbs_workspace_bytes)")
     if out is None:
         out = torch.empty((count, P.k * P.N + 1), dtype=torch.int64, device=lwe_in.device)
