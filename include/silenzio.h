@@ -344,6 +344,11 @@ long silenzio_pbs_trace_end(int kind, uint64_t *elements_seen);
  * rounded since the last call (R20: exact while < 1/2 and < 2^51);
  * resets both. Release builds return SILENZIO_ERR_UNSUPPORTED. */
 int silenzio_debug_fft_margin(double *max_frac, double *max_abs);
+/* Debug builds only (-DSZ_PHASE_TIMING=1, tools/phase_times.py): clock64 cycles
+ * accumulated per phase of the set-A CMux loop, out[warp][phase] (8 x 8, CTA 0,
+ * phases: publish, digits, forward FFT, spectra exchange, stage wait, MAC,
+ * inverse FFT, recombination); resets them. Release builds: UNSUPPORTED. */
+int silenzio_debug_phase_times(unsigned long long *out);
 
 #ifdef __cplusplus
 }

@@ -38,7 +38,6 @@ constexpr int kN = 2048;
 constexpr int kLog2_2N = 12;
 constexpr int kM = 1024;
 constexpr int kCts = 4;       // ciphertexts per CTA
-constexpr int kThreads = 256;  // 8 warps
 constexpr uint32_t kTmemCols = 512;
 
 // cos(2 pi e / 32), e = 0..31 (correctly rounded doubles)
@@ -166,10 +165,12 @@ __device__ __forceinline__ double2 untwist_unscaled(double2 a) {
 // over every rounded limb value of the launch (R20: exactness needs
 // |error| < 1/2 and |x| < 2^51)
 __device__ unsigned long long g_margin_frac, g_margin_abs;
-__device__ __forceinline__ void margin_note(double x, u64 bits) {
+// x = u * s (the untwisted limb value, never rounded on its own: the kernel
+// rounds fma(u, s, 1.5 * 2^52)); |u s - round| with one rounding
+__device__ __forceinline__ void margin_note(double u, double s, u64 bits) {
   const double r = __longlong_as_double((long long)bits) - 6755399441055744.0;  // round(x), exact
-  unsigned long long f = (unsigned long long)__double_as_longlong(fabs(x - r));
-  unsigned long long a = (unsigned long long)__double_as_longlong(fabs(x));
+  unsigned long long f = (unsigned long long)__double_as_longlong(fabs(fma(u, s, -r)));
+  unsigned long long a = (unsigned long long)__double_as_longlong(fabs(u * s));
   // warp-level max first (one atomic per warp)
   for (int d = 16; d; d >>= 1) {
     f = max(f, (unsigned long long)__shfl_xor_sync(0xffffffffu, f, d));
@@ -188,8 +189,8 @@ __device__ __forceinline__ void untwist_round_t(double2 y, u64 &bx, u64 &by) {
   bx = (u64)__double_as_longlong(fma(u.x, s, 6755399441055744.0));
   by = (u64)__double_as_longlong(fma(u.y, s, 6755399441055744.0));
 #if SZ_FFT_MARGIN
-  margin_note(u.x * s, bx);
-  margin_note(u.y * s, by);
+  margin_note(u.x, s, bx);
+  margin_note(u.y, s, by);
 #endif
 }
 __device__ __forceinline__ void untwist_round(double2 y, int m, u64 &bx, u64 &by) {
@@ -350,11 +351,23 @@ struct Args {
 };
 
 __host__ __device__ constexpr size_t abar_bytes(int n) { return ((size_t)n * 2 + 15) / 16 * 16; }
-__host__ __device__ constexpr size_t smem_bytes(int n) {
-  return 8 * (size_t)kXbuf * sizeof(double2)  // per-warp transposition buffers (also the ACC copy)
-         + 4 * (size_t)kM * sizeof(double2)  // BSK stage: one (i, limb), [o][row][32][32]
-         + kCts * abar_bytes(n)              // modswitched masks
-         + 16;                               // mbarrier
+// Two layouts of the same kernel:
+//  SMALL = false: 4 ciphertexts, 8 warps; ciphertext s on warps s (mask) and
+//    s + 4 (body), which share TMEM lane quadrant s, so the digit spectra are
+//    exchanged through tensor memory (the throughput layout);
+//  SMALL = true: 2 ciphertexts, 4 warps; ciphertext s on warps s and s + 2, i.e.
+//    on two different schedulers (one FP64 pipe each), the spectra exchanged
+//    through shared memory: a batch of <= 2 x SMs ciphertexts runs at half the
+//    CMux latency of the throughput layout.
+template <bool SMALL> struct Lay {
+  static constexpr int cts = SMALL ? 2 : 4, warps = 2 * cts, threads = 32 * warps;
+};
+__host__ __device__ constexpr size_t smem_bytes(int n, bool small = false) {
+  return (small ? 4 : 8) * (size_t)kXbuf * sizeof(double2)  // per-warp transposition buffers (also the ACC copy)
+         + 4 * (size_t)kM * sizeof(double2)                  // BSK stage: one (i, limb), [o][row][32][32]
+         + (small ? 2 * 2 * (size_t)kM * sizeof(double2) : 0)  // SMALL: digit spectra [slot][row][1024]
+         + (small ? 2 : kCts) * abar_bytes(n)                // modswitched masks
+         + 16;                                               // mbarrier
 }
 
 __device__ __forceinline__ u64 acc_init(const u64 *v, int j, int bt, int g) {
@@ -388,18 +401,41 @@ __device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[kCQ][
 
 constexpr u64 kMagicBits = 0x4338000000000000ull;  // bits of 1.5 * 2^52
 
-template <int P>
-__global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) {
+#ifndef SZ_PHASE_TIMING
+#define SZ_PHASE_TIMING 0  // 1: debug build accumulating clock64 per CMux phase (CTA 0, lane 0 of each warp)
+#endif
+#if SZ_PHASE_TIMING
+__device__ unsigned long long g_phase[8][8];
+#define SZ_PT_INIT long long sz_pt_prev = clock64();
+#define SZ_PT(k)                                                        \
+  do {                                                                  \
+    if (blockIdx.x == 0 && lane == 0) {                                 \
+      const long long now = clock64();                                  \
+      atomicAdd(&g_phase[wid][k], (unsigned long long)(now - sz_pt_prev)); \
+      sz_pt_prev = now;                                                 \
+    }                                                                   \
+  } while (0)
+#else
+#define SZ_PT_INIT
+#define SZ_PT(k) \
+  do {           \
+  } while (0)
+#endif
+
+template <int P, bool SMALL>
+__global__ void __launch_bounds__(Lay<SMALL>::threads, 1) blind_rotate_warp_kernel(Args A) {
+  constexpr int kC = Lay<SMALL>::cts, kW = Lay<SMALL>::warps;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t tmem_slot;
-  __shared__ uint32_t mac_done;  // warps finished with the staged limb, monotone (the 8th of a round re-arms)
+  __shared__ uint32_t mac_done;  // warps finished with the staged limb, monotone (the kW-th of a round re-arms)
   const int n = A.n, w = A.w, blog = A.base_log;
   double2 *xbuf_all = reinterpret_cast<double2 *>(smem);
-  double2 *gbuf = xbuf_all + 8 * kXbuf;
-  unsigned char *abar_base = reinterpret_cast<unsigned char *>(gbuf + 4 * kM);
-  uint64_t *mbar = reinterpret_cast<uint64_t *>(abar_base + kCts * abar_bytes(n));
+  double2 *gbuf = xbuf_all + kW * kXbuf;
+  double2 *dsm = gbuf + 4 * kM;  // SMALL: digit spectra [slot][row][32 r][32 lane]
+  unsigned char *abar_base = reinterpret_cast<unsigned char *>(dsm + (SMALL ? 2 * 2 * kM : 0));
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(abar_base + kC * abar_bytes(n));
   const int tid = threadIdx.x, wid = tid >> 5, lane = tid & 31;
-  const int cs = wid & 3, g = wid >> 2;  // ciphertext slot, GLWE component
+  const int cs = wid % kC, g = wid / kC;  // ciphertext slot, GLWE component
   double2 *xbuf = xbuf_all + wid * kXbuf;
   ulonglong2 *accp = reinterpret_cast<ulonglong2 *>(xbuf);  // ACC_g copy as [1024] coefficient pairs
   unsigned short *abar = reinterpret_cast<unsigned short *>(abar_base + cs * abar_bytes(n));
@@ -410,8 +446,12 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  const uint32_t tl = tmem_slot + ((uint32_t)(32 * cs) << 16);
-  const uint32_t ta_acc = tl + 128 * g, ta_d0 = tl + 256, ta_d1 = tl + 384, ta_dg = tl + 256 + 128 * g;
+  // TMEM: lane quadrant = warp % 4. Throughput layout: quadrant cs holds
+  // ACC_0 | ACC_1 | D^_0 | D^_1 of ciphertext cs; SMALL: quadrant wid holds ACC_g.
+  const uint32_t tl = tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16);
+  const uint32_t ta_acc = tl + (SMALL ? 0 : 128 * g), ta_d0 = tl + 256, ta_d1 = tl + 384,
+                 ta_dg = tl + 256 + 128 * g;
+  double2 *dsm_s = dsm + (size_t)cs * 2 * kM;  // SMALL: this slot's [row][r][lane]
   const uint32_t limb_bytes = 4 * kM * sizeof(double2);
   auto issue = [&](int i, int p) {
     bulk_load(gbuf, A.fbsk + ((size_t)i * P + p) * 4 * kM, limb_bytes, mbar);
@@ -419,10 +459,10 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
   uint32_t round = 0;  // completed bulk copies (mbarrier phase parity)
   const u64 half_q = 1ull << (63 - blog);
 
-  const long ngroups = (A.count + kCts - 1) / kCts;
+  const long ngroups = (A.count + kC - 1) / kC;
   for (long grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     if (tid == 0) issue(0, P - 1);
-    const long c_raw = grp * kCts + cs;
+    const long c_raw = grp * kC + cs;
     const bool live = c_raw < A.count;
     const long c = live ? c_raw : A.count - 1;  // idle slots replay the last ciphertext
     const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
@@ -445,6 +485,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
     tmem_wait_st();
     __syncthreads();  // abar visible
 
+    SZ_PT_INIT
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
       // ---------------- publish ACC_g for the rotation, as coefficient pairs
@@ -458,6 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
         for (int q = 0; q < kCQ; q++) accp[lane + 32 * (kCQ * cc + q)] = make_ulonglong2(a4[q][0], a4[q][1]);
       }
       __syncwarp();
+      SZ_PT(0);
       // ---------------- digits of X^a ACC_g - ACC_g (a4.1-a4.2), forward FFT
       // (X^a ACC)[j] = +-ACC[(j - a) mod 2N]: for j0 = lane + 32 m and j1 = j0 + 1024,
       // src0 = (j0 - a) mod 4096 = 1024 qd + s picks the pair accp[s] for both:
@@ -482,54 +524,76 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
                                          (double)((i64)(r1 - a4[q][1] + half_q) >> (64 - blog)));
         }
       }
+      SZ_PT(1);
       fwd_fft32(x, xbuf, lane);
+      SZ_PT(2);
       if (i > 0) {  // both warps of the ciphertext are past the previous CMux's MACs (D^ reads)
         tmem_fence_before();
         asm volatile("bar.sync %0, %1;" ::"r"(5 + cs), "r"(64) : "memory");
         tmem_fence_after();
       }
+      if constexpr (SMALL) {
 #pragma unroll
-      for (int jj = 0; jj < 8; jj++) {
-        uint32_t r16[16];
-        pack4(&x[4 * jj], r16);
-        tmem_st16(ta_dg + 16 * jj, r16);
+        for (int k2 = 0; k2 < 32; k2++) dsm_s[g * kM + 32 * k2 + lane] = x[k2];
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + cs), "r"(64) : "memory");  // D^_0 and D^_1 written
+      } else {
+#pragma unroll
+        for (int jj = 0; jj < 8; jj++) {
+          uint32_t r16[16];
+          pack4(&x[4 * jj], r16);
+          tmem_st16(ta_dg + 16 * jj, r16);
+        }
+        tmem_wait_st();
+        tmem_fence_before();
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + cs), "r"(64) : "memory");  // D^_0 and D^_1 written
+        tmem_fence_after();
       }
-      tmem_wait_st();
-      tmem_fence_before();
-      asm volatile("bar.sync %0, %1;" ::"r"(1 + cs), "r"(64) : "memory");  // D^_0 and D^_1 written
-      tmem_fence_after();
+      SZ_PT(3);
       // ---------------- per limb: MAC with the staged BSK, inverse FFT, exact ACC update
 #pragma unroll 1
       for (int p = P - 1; p >= 0; p--) {
         mbar_wait(mbar, round & 1);
         round++;
+        SZ_PT(4);
         double2 y[32];
         const double2 *G0 = gbuf + (size_t)(2 * g) * kM + lane;  // [o = g][row 0]
         const double2 *G1 = G0 + kM;                             // [o = g][row 1]
+        if constexpr (SMALL) {
 #pragma unroll
-        for (int jj = 0; jj < 4; jj++) {
-          uint32_t d0[32], d1[32];
-          tmem_ld32(ta_d0 + 32 * jj, d0);
-          tmem_ld32(ta_d1 + 32 * jj, d1);
-          tmem_wait_ld32x2(d0, d1);
-#pragma unroll
-          for (int q = 0; q < 8; q++) {
-            const int r = 8 * jj + q;
+          for (int r = 0; r < 32; r++) {
             double2 acc = make_double2(0.0, 0.0);
-            cmac(acc, unpack1(d0, q), G0[r * 32]);
-            cmac(acc, unpack1(d1, q), G1[r * 32]);
+            cmac(acc, dsm_s[32 * r + lane], G0[r * 32]);
+            cmac(acc, dsm_s[kM + 32 * r + lane], G1[r * 32]);
             y[r] = acc;
           }
+        } else {
+#pragma unroll
+          for (int jj = 0; jj < 4; jj++) {
+            uint32_t d0[32], d1[32];
+            tmem_ld32(ta_d0 + 32 * jj, d0);
+            tmem_ld32(ta_d1 + 32 * jj, d1);
+            tmem_wait_ld32x2(d0, d1);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              const int r = 8 * jj + q;
+              double2 acc = make_double2(0.0, 0.0);
+              cmac(acc, unpack1(d0, q), G0[r * 32]);
+              cmac(acc, unpack1(d1, q), G1[r * 32]);
+              y[r] = acc;
+            }
+          }
         }
-        // this warp is done with the stage; the 8th warp of the round re-arms it
+        SZ_PT(5);
+        // this warp is done with the stage; the last warp of the round re-arms it
         // with the next (i, limb) -- no CTA-wide barrier
         __syncwarp();
-        if (lane == 0 && (stage_release(&mac_done) & 7) == 7) {
+        if (lane == 0 && (stage_release(&mac_done) % kW) == kW - 1) {
           if (p > 0) issue(i, p - 1);
           else if (i + 1 < n) issue(i + 1, P - 1);
         }
         constexpr bool kFusedUntwist = (P == 3);
         inv_fft32<!kFusedUntwist>(y, xbuf, lane);
+        SZ_PT(6);
         // P = 3: bits(x + 1.5 2^52) << 22p per limb, the magic constant's share of
         // all three limbs removed once per CMux (at p = 0)
         const u64 limb_off = (p == 0) ? kMagicBits + (kMagicBits << w) + (kMagicBits << (2 * w)) : 0ull;
@@ -552,6 +616,7 @@ __global__ void __launch_bounds__(kThreads, 1) blind_rotate_warp_kernel(Args A) 
           acc_st(ta_acc, cc, a4);
         }
         tmem_wait_st();
+        SZ_PT(7);
       }
     }
     // ---- sample extraction (a5): a'[0] = A[0], a'[i] = -A[N-i], b' = B[0]
@@ -799,6 +864,21 @@ long blind_rotate_warp_wave() {
 
 long blind_rotate_warp_launches(size_t count) { return count ? 1 : 0; }
 
+// SZ_PHASE_TIMING debug builds: clock64 cycles per phase [warp][phase] of CTA 0
+// (0 publish, 1 digits, 2 forward FFT, 3 spectra exchange, 4 stage wait, 5 MAC,
+// 6 inverse FFT, 7 recombination), read and reset
+extern "C" int silenzio_debug_phase_times(unsigned long long *out /* [8][8] */) {
+#if SZ_PHASE_TIMING
+  unsigned long long z[64] = {0};
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(out, w32::g_phase, sizeof(z)));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_phase, z, sizeof(z)));
+  return SILENZIO_OK;
+#else
+  (void)out;
+  return SILENZIO_ERR_UNSUPPORTED;
+#endif
+}
+
 // SZ_FFT_MARGIN debug builds: read-and-reset the recorded rounding margin
 extern "C" int silenzio_debug_fft_margin(double *max_frac, double *max_abs) {
 #if SZ_FFT_MARGIN
@@ -820,23 +900,30 @@ extern "C" int silenzio_debug_fft_margin(double *max_frac, double *max_abs) {
 #endif
 }
 
-// Largest batch the latency kernel takes (one ciphertext per SM per wave):
-// up to SZ_LAT_WAVES waves of it beat one launch of the four-ciphertext kernel
-// (measured). SZ_LAT_WAVES = 0 disables it.
+// Largest batch the latency kernel takes (one ciphertext per SM): one wave of
+// it (8.1-8.9 ms) beats both other layouts up to SMs ciphertexts; two waves do
+// not (measured, tools/ab_lat.sh). SZ_LAT_WAVES = 0 disables it.
 #ifndef SZ_LAT_WAVES
-#define SZ_LAT_WAVES 3
+#define SZ_LAT_WAVES 1
 #endif
 long blind_rotate_lat_max(long sms) { return SZ_LAT_WAVES * sms; }
+// Largest batch the SMALL layout (two ciphertexts per CTA, four warps) takes:
+// one wave of it, 2 x SMs ciphertexts (10.9 ms vs 12.6 ms for the four-
+// ciphertext layout; SZ_SMALL_WAVES = 0 disables it).
+#ifndef SZ_SMALL_WAVES
+#define SZ_SMALL_WAVES 1
+#endif
+long blind_rotate_small_max(long sms) { return SZ_SMALL_WAVES * 2 * sms; }
 
 int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64 *luts, u32 num_luts,
                              const void *fbsk, u64 *lwe_out, size_t count, const silenzio_params *P,
                              cudaStream_t stream) {
   int st = w32::ensure_tables();
   if (st != SILENZIO_OK) return st;
-  void (*kern)(w32::Args) = nullptr;
-  if (P->fft_limbs == 1) kern = w32::blind_rotate_warp_kernel<1>;
-  if (P->fft_limbs == 2) kern = w32::blind_rotate_warp_kernel<2>;
-  if (P->fft_limbs == 3) kern = w32::blind_rotate_warp_kernel<3>;
+  void (*kern)(w32::Args) = nullptr, (*kern_s)(w32::Args) = nullptr;
+  if (P->fft_limbs == 1) kern = w32::blind_rotate_warp_kernel<1, false>, kern_s = w32::blind_rotate_warp_kernel<1, true>;
+  if (P->fft_limbs == 2) kern = w32::blind_rotate_warp_kernel<2, false>, kern_s = w32::blind_rotate_warp_kernel<2, true>;
+  if (P->fft_limbs == 3) kern = w32::blind_rotate_warp_kernel<3, false>, kern_s = w32::blind_rotate_warp_kernel<3, true>;
   if (!kern) return SILENZIO_ERR_UNSUPPORTED;
   w32::Args A;
   A.lwe_small = lwe_small;
@@ -853,7 +940,7 @@ int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64
   if (wave <= 0) return SILENZIO_ERR_CUDA;
   const long sms = wave / w32::kCts;
   if ((long)count <= blind_rotate_lat_max(sms) && w32::lat_smem_bytes(A.n) <= 227 * 1024) {
-    // small batch: one ciphertext per CTA, the eight FFTs of a CMux on eight warps
+    // at most one ciphertext per SM: the eight FFTs of a CMux on eight warps
     void (*lk)(w32::Args) = nullptr;
     if (P->fft_limbs == 1) lk = w32::blind_rotate_lat_kernel<1>;
     if (P->fft_limbs == 2) lk = w32::blind_rotate_lat_kernel<2>;
@@ -862,6 +949,16 @@ int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64
     SZ_CUDA_OK(cudaFuncSetAttribute(lk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsmem));
     const long grid = (long)count < sms ? (long)count : sms;
     lk<<<(unsigned)grid, w32::kLatThreads, lsmem, stream>>>(A);
+    SZ_LAUNCH_OK();
+    return SILENZIO_OK;
+  }
+  if ((long)count <= blind_rotate_small_max(sms) && w32::smem_bytes(A.n, true) <= 227 * 1024) {
+    // small batch: two ciphertexts per CTA on four warps (one scheduler each)
+    const size_t ssmem = w32::smem_bytes(A.n, true);
+    SZ_CUDA_OK(cudaFuncSetAttribute(kern_s, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssmem));
+    const long groups = ((long)count + 1) / 2;
+    const long grid = groups < sms ? groups : sms;
+    kern_s<<<(unsigned)grid, w32::Lay<true>::threads, ssmem, stream>>>(A);
     SZ_LAUNCH_OK();
     return SILENZIO_OK;
   }
@@ -875,7 +972,7 @@ int launch_blind_rotate_warp(const u64 *lwe_small, const u32 *lut_ids, const u64
   // (DESIGN.md §8).
   const long groups = ((long)count + w32::kCts - 1) / w32::kCts;
   const long grid = groups < wave / w32::kCts ? groups : wave / w32::kCts;
-  kern<<<(unsigned)grid, w32::kThreads, smem, stream>>>(A);
+  kern<<<(unsigned)grid, w32::Lay<false>::threads, smem, stream>>>(A);
   SZ_LAUNCH_OK();
   return SILENZIO_OK;
 }

@@ -69,3 +69,31 @@ def gather_channels(local: torch.Tensor, k: int, world: int, rank: int) -> torch
         idx = list(range(r, k, world))
         out[idx] = parts[r][: len(idx)]
     return out
+
+
+# Output-tile sharding of Matmul^RNS (SURVEY.md §8(e) "or by output tile"):
+# rank r computes the rows [lo, hi) of X W for every modulus. Every row costs
+# the same number of PBS, so any world size up to the row count is balanced
+# (modulus sharding caps at k ranks and is unbalanced: m in {9, 11, 13} cost
+# 4 PBS per product, {5, 7} 2). One all-gather returns the full output.
+def shard_rows(a: int, world: int, rank: int):
+    """Rows [lo, hi) of the a-row output owned by `rank`."""
+    return shard_bounds(a, world, rank)
+
+
+def gather_rows(local: torch.Tensor, a: int, world: int, rank: int) -> torch.Tensor:
+    """local [k][rows of this rank][c][...] -> [k][a][c][...] on every rank
+    (all_gather of equal-sized, zero-padded slabs, rows back in order)."""
+    per = (a + world - 1) // world
+    shape = (local.shape[0], per) + tuple(local.shape[2:])
+    slab = torch.zeros(shape, dtype=local.dtype, device=local.device)
+    slab[:, : local.shape[1]] = local
+    if world == 1:
+        return slab[:, :a].clone()
+    parts = [torch.empty_like(slab) for _ in range(world)]
+    dist.all_gather(parts, slab)
+    out = torch.empty((local.shape[0], a) + tuple(local.shape[2:]), dtype=local.dtype, device=local.device)
+    for r in range(world):
+        lo, hi = shard_rows(a, world, r)
+        out[:, lo:hi] = parts[r][:, : hi - lo]
+    return out

@@ -79,6 +79,7 @@ def load():
         "silenzio_pbs_trace_begin": ([I, V, S, ctypes.c_uint64, ctypes.c_uint64, S, S, S], I),
         "silenzio_pbs_trace_end": ([I, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_long),
         "silenzio_debug_fft_margin": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], I),
+        "silenzio_debug_phase_times": ([V], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -102,7 +103,7 @@ def exported_symbols():
         "silenzio_shift2msbs_workspace_bytes", "silenzio_shift2msbs_pm",
         "silenzio_train_workspace_bytes", "silenzio_channel16", "silenzio_rns_sign3", "silenzio_relu_cap",
         "silenzio_relu_mask", "silenzio_weight_update", "silenzio_pbs_trace_begin", "silenzio_pbs_trace_end",
-        "silenzio_debug_fft_margin",
+        "silenzio_debug_fft_margin", "silenzio_debug_phase_times",
     ]
 
 

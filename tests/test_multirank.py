@@ -106,3 +106,42 @@ def test_two_rank_modulus_sharding():
     assert sorted(res[0][1] + res[1][1]) == list(range(6))
     for _, _, order in res:
         assert order == [5, 7, 9, 11, 13, 16]
+
+
+def _worker_rows(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        k, a, c = 6, 5, 3
+        lo, hi = sdist.shard_rows(a, world, rank)
+        # stand-in for this rank's Matmul^RNS output rows: values tagged (modulus index, row, col)
+        local = torch.tensor([[[100 * mi + 10 * row + col for col in range(c)] for row in range(lo, hi)]
+                              for mi in range(k)], dtype=torch.int64).reshape(k, hi - lo, c, 1)
+        full = sdist.gather_rows(local, a, world, rank)
+        q.put((rank, (lo, hi), full.reshape(k, a, c).tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_output_row_sharding():
+    """Config-3 sharding by output tile: the ranks' row blocks
+    partition the 5 output rows (uneven split), and the all-gather returns the
+    full [k][a][c] output, rows in order, on every rank."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker_rows, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][1] == (0, 3) and res[1][1] == (3, 5)
+    want = [[[100 * mi + 10 * row + col for col in range(3)] for row in range(5)] for mi in range(6)]
+    for _, _, full in res:
+        assert full == want
+    # 16 rows over 8 ranks (configs[3] on 8 GPUs): 2 rows each
+    assert [sdist.shard_rows(16, 8, r)[1] - sdist.shard_rows(16, 8, r)[0] for r in range(8)] == [2] * 8

@@ -16,8 +16,9 @@ from synth import get_params, key_randomness, lwe_randomness, streams  # noqa: E
 
 a, b, c = [int(v) for v in (sys.argv[1:4] if len(sys.argv) >= 4 else (16, 784, 64))]
 BASE = [5, 7, 9, 11, 13, 16]
-# multi-GPU (torchrun): the modulus channels are sharded over the ranks
-# (SURVEY.md §8(e)); keys and inputs are replicated from the same seeds
+# multi-GPU (torchrun): the output rows (default) or the modulus channels
+# (SILENZIO_SHARD=moduli) are sharded over the ranks; keys and
+# inputs are replicated from the same seeds; one all-gather at the end
 from paper_2504_17785_b200 import dist as sdist  # noqa: E402
 WORLD, RANK = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
 if WORLD > 1:
@@ -39,12 +40,18 @@ torch.cuda.synchronize()
 t0 = time.perf_counter()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
-_, my_mods = sdist.shard_moduli(BASE, WORLD, RANK)
-local = silenzio.rns_matmul(Xc, Wc, my_mods, keys["fbsk"], keys["ksk"], P)
+SHARD = os.environ.get("SILENZIO_SHARD", "rows")  # rows: output-row tiles (default); moduli: RNS channels
+if SHARD == "moduli":
+    _, my_mods = sdist.shard_moduli(BASE, WORLD, RANK)
+    local = silenzio.rns_matmul(Xc, Wc, my_mods, keys["fbsk"], keys["ksk"], P)
+else:
+    lo, hi = sdist.shard_rows(a, WORLD, RANK)
+    local = silenzio.rns_matmul(Xc[lo:hi].contiguous(), Wc, BASE, keys["fbsk"], keys["ksk"], P)
 e1.record()
 torch.cuda.synchronize()
 ms = sdist.max_over_ranks(e0.elapsed_time(e1), device=dev)
-out = sdist.gather_channels(local, len(BASE), WORLD, RANK)
+out = (sdist.gather_channels(local, len(BASE), WORLD, RANK) if SHARD == "moduli"
+       else sdist.gather_rows(local, a, WORLD, RANK))
 torch.cuda.synchronize()
 wall = time.perf_counter() - t0
 if RANK != 0:
@@ -68,6 +75,6 @@ ref = X @ W
 mism = int((val != ref).sum())
 pbs = (a * b + b * c) * 7 + a * b * c * (2 + 2 + 4 * 3 + 3)
 print(json.dumps({"workload": f"configs[3] Matmul^RNS {a}x{b} . {b}x{c}, base {BASE}, set A",
-                  "n_gpus": WORLD, "sharding": "modulus channels round-robin over ranks",
+                  "n_gpus": WORLD, "sharding": ("modulus channels round-robin over ranks" if SHARD == "moduli" else "output rows in contiguous blocks over ranks"),
                   "gadget_layer_s": ms / 1e3, "wall_s": wall, "outputs": int(res.size),
                   "crt_mismatches": mism, "max_abs_xw": int(np.abs(ref).max())}))
