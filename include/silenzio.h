@@ -339,11 +339,13 @@ int silenzio_pbs_trace_begin(int kind, uint64_t *records, size_t max_records, ui
                              size_t in_words, size_t out_words, size_t lut_words);
 long silenzio_pbs_trace_end(int kind, uint64_t *elements_seen);
 
-/* Debug builds only (-DSZ_FFT_MARGIN=1, tools/fft_margin.py): the largest
- * |x - round(x)| and |x| over every limb value the set-A blind rotations
- * rounded since the last call (R20: exact while < 1/2 and < 2^51);
- * resets both. Release builds return SILENZIO_ERR_UNSUPPORTED. */
-int silenzio_debug_fft_margin(double *max_frac, double *max_abs);
+/* Debug builds only (-DSZ_FFT_MARGIN=1, tools/fft_margin.py): per limb p < 3,
+ * over every limb value the set-A blind rotations rounded since the last call
+ * (R20: exact while the FFT error < 1/2 and |x| < 2^51):
+ * out[4p] = max |x - round(x)|, out[4p+1] = max |x|, out[4p+2] = number of
+ * values with |x - round(x)| >= 1/4, out[4p+3] = number >= 1/2; resets them.
+ * Release builds return SILENZIO_ERR_UNSUPPORTED. */
+int silenzio_debug_fft_margin(double *out);
 /* Debug builds only (-DSZ_PHASE_TIMING=1, tools/phase_times.py): clock64 cycles
  * accumulated per phase of the set-A CMux loop, out[warp][phase] (8 x 8, CTA 0,
  * phases: publish, digits, forward FFT, spectra exchange, stage wait, MAC,

@@ -161,42 +161,48 @@ __device__ __forceinline__ double2 untwist_unscaled(double2 a) {
 #define SZ_FFT_MARGIN 0  // 1: debug build recording the rounding margin of every limb (tools/fft_margin.py)
 #endif
 #if SZ_FFT_MARGIN
-// max |x - round(x)| (as f64 bits: non-negative doubles order like u64) and max |x|
-// over every rounded limb value of the launch (R20: exactness needs
-// |error| < 1/2 and |x| < 2^51)
-__device__ unsigned long long g_margin_frac, g_margin_abs;
+// per limb p: max |x - round(x)| and max |x| (f64 bits: non-negative doubles
+// order like u64) and the count of values with |x - round(x)| >= 1/4 and >= 1/2
+// over every rounded limb value (R20: exact while the FFT error
+// stays below 1/2 and |x| < 2^51)
+__device__ unsigned long long g_margin_frac[3], g_margin_abs[3], g_margin_q[3], g_margin_h[3];
 // x = u * s (the untwisted limb value, never rounded on its own: the kernel
 // rounds fma(u, s, 1.5 * 2^52)); |u s - round| with one rounding
-__device__ __forceinline__ void margin_note(double u, double s, u64 bits) {
+__device__ __forceinline__ void margin_note(double u, double s, u64 bits, int p) {
   const double r = __longlong_as_double((long long)bits) - 6755399441055744.0;  // round(x), exact
-  unsigned long long f = (unsigned long long)__double_as_longlong(fabs(fma(u, s, -r)));
+  const double fr = fabs(fma(u, s, -r));
+  unsigned long long f = (unsigned long long)__double_as_longlong(fr);
   unsigned long long a = (unsigned long long)__double_as_longlong(fabs(u * s));
-  // warp-level max first (one atomic per warp)
-  for (int d = 16; d; d >>= 1) {
+  unsigned q = __popc(__ballot_sync(0xffffffffu, fr >= 0.25)), h = __popc(__ballot_sync(0xffffffffu, fr >= 0.5));
+  for (int d = 16; d; d >>= 1) {  // warp-level max first (one atomic per warp)
     f = max(f, (unsigned long long)__shfl_xor_sync(0xffffffffu, f, d));
     a = max(a, (unsigned long long)__shfl_xor_sync(0xffffffffu, a, d));
   }
   if ((threadIdx.x & 31) == 0) {
-    atomicMax(&g_margin_frac, f);
-    atomicMax(&g_margin_abs, a);
+    atomicMax(&g_margin_frac[p], f);
+    atomicMax(&g_margin_abs[p], a);
+    if (q) atomicAdd(&g_margin_q[p], (unsigned long long)q);
+    if (h) atomicAdd(&g_margin_h[p], (unsigned long long)h);
   }
 }
 #endif
 template <int M>
-__device__ __forceinline__ void untwist_round_t(double2 y, u64 &bx, u64 &by) {
+__device__ __forceinline__ void untwist_round_t(double2 y, u64 &bx, u64 &by, int p) {
   const double2 u = untwist_unscaled<M>(y);
   constexpr double s = twist_scale(M);
   bx = (u64)__double_as_longlong(fma(u.x, s, 6755399441055744.0));
   by = (u64)__double_as_longlong(fma(u.y, s, 6755399441055744.0));
 #if SZ_FFT_MARGIN
-  margin_note(u.x, s, bx);
-  margin_note(u.y, s, by);
+  margin_note(u.x, s, bx, p);
+  margin_note(u.y, s, by, p);
+#else
+  (void)p;
 #endif
 }
-__device__ __forceinline__ void untwist_round(double2 y, int m, u64 &bx, u64 &by) {
+__device__ __forceinline__ void untwist_round(double2 y, int m, u64 &bx, u64 &by, int p) {
   switch (m & 31) {
 #define SZ_U(k) \
-  case k: untwist_round_t<k>(y, bx, by); break;
+  case k: untwist_round_t<k>(y, bx, by, p); break;
     SZ_U(0) SZ_U(1) SZ_U(2) SZ_U(3) SZ_U(4) SZ_U(5) SZ_U(6) SZ_U(7)
     SZ_U(8) SZ_U(9) SZ_U(10) SZ_U(11) SZ_U(12) SZ_U(13) SZ_U(14) SZ_U(15)
     SZ_U(16) SZ_U(17) SZ_U(18) SZ_U(19) SZ_U(20) SZ_U(21) SZ_U(22) SZ_U(23)
@@ -605,7 +611,7 @@ __global__ void __launch_bounds__(Lay<SMALL>::threads, 1) blind_rotate_warp_kern
           for (int q = 0; q < kCQ; q++) {
             if constexpr (kFusedUntwist) {
               u64 bx, by;
-              untwist_round(y[kCQ * cc + q], kCQ * cc + q, bx, by);
+              untwist_round(y[kCQ * cc + q], kCQ * cc + q, bx, by, p);
               a4[q][0] += (bx << (p * w)) - limb_off;
               a4[q][1] += (by << (p * w)) - limb_off;
             } else {
@@ -794,7 +800,7 @@ __global__ void __launch_bounds__(kLatThreads, 1) blind_rotate_lat_kernel(Args A
 #pragma unroll
             for (int m = 0; m < 32; m++) {
               u64 bx, by;
-              untwist_round(y[m], m, bx, by);
+              untwist_round(y[m], m, bx, by, p);
               contrib[lane + 32 * m] = make_ulonglong2((bx << (p * w)) - off, (by << (p * w)) - off);
             }
           } else {
@@ -879,23 +885,30 @@ extern "C" int silenzio_debug_phase_times(unsigned long long *out /* [8][8] */) 
 #endif
 }
 
-// SZ_FFT_MARGIN debug builds: read-and-reset the recorded rounding margin
-extern "C" int silenzio_debug_fft_margin(double *max_frac, double *max_abs) {
+// SZ_FFT_MARGIN debug builds: read-and-reset the recorded rounding margin, per
+// limb p < 3: out[4 p + 0] = max |x - round(x)|, [4 p + 1] = max |x|,
+// [4 p + 2] = count |x - round(x)| >= 1/4, [4 p + 3] = count >= 1/2
+extern "C" int silenzio_debug_fft_margin(double *out /* [12] */) {
 #if SZ_FFT_MARGIN
-  unsigned long long f = 0, a = 0, z = 0;
-  SZ_CUDA_OK(cudaMemcpyFromSymbol(&f, w32::g_margin_frac, 8));
-  SZ_CUDA_OK(cudaMemcpyFromSymbol(&a, w32::g_margin_abs, 8));
-  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_frac, &z, 8));
-  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_abs, &z, 8));
-  double df, da;
-  memcpy(&df, &f, 8);
-  memcpy(&da, &a, 8);
-  if (max_frac) *max_frac = df;
-  if (max_abs) *max_abs = da;
+  unsigned long long f[3], a[3], q[3], h[3], z[3] = {0, 0, 0};
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(f, w32::g_margin_frac, sizeof(f)));
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(a, w32::g_margin_abs, sizeof(a)));
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(q, w32::g_margin_q, sizeof(q)));
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(h, w32::g_margin_h, sizeof(h)));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_frac, z, sizeof(z)));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_abs, z, sizeof(z)));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_q, z, sizeof(z)));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(w32::g_margin_h, z, sizeof(z)));
+  if (out)
+    for (int p = 0; p < 3; p++) {
+      memcpy(&out[4 * p], &f[p], 8);
+      memcpy(&out[4 * p + 1], &a[p], 8);
+      out[4 * p + 2] = (double)q[p];
+      out[4 * p + 3] = (double)h[p];
+    }
   return SILENZIO_OK;
 #else
-  (void)max_frac;
-  (void)max_abs;
+  (void)out;
   return SILENZIO_ERR_UNSUPPORTED;
 #endif
 }

@@ -78,7 +78,7 @@ def load():
         "silenzio_weight_update": ([V, V, S, ctypes.c_int32, ctypes.c_int32, V, V, V, P, V, S, V], I),
         "silenzio_pbs_trace_begin": ([I, V, S, ctypes.c_uint64, ctypes.c_uint64, S, S, S], I),
         "silenzio_pbs_trace_end": ([I, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_long),
-        "silenzio_debug_fft_margin": ([ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)], I),
+        "silenzio_debug_fft_margin": ([V], I),
         "silenzio_debug_phase_times": ([V], I),
     }
     for name, (args, res) in sigs.items():
@@ -527,8 +527,9 @@ class PbsTrace:
 
 
 def debug_fft_margin():
-    """(max |x - round(x)|, max |x|) over the limbs rounded since the last call
-    (debug builds with -DSZ_FFT_MARGIN=1 only)."""
-    f, a = ctypes.c_double(0), ctypes.c_double(0)
-    _check(load().silenzio_debug_fft_margin(ctypes.byref(f), ctypes.byref(a)))
-    return f.value, a.value
+    """Per limb p: dict(max_frac, max_abs, n_ge_quarter, n_ge_half) over the limbs
+    rounded since the last call (debug builds with -DSZ_FFT_MARGIN=1 only)."""
+    out = (ctypes.c_double * 12)()
+    _check(load().silenzio_debug_fft_margin(out))
+    return [dict(max_frac=out[4 * p], max_abs=out[4 * p + 1], n_ge_quarter=int(out[4 * p + 2]),
+                 n_ge_half=int(out[4 * p + 3])) for p in range(3)]

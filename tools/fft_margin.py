@@ -35,15 +35,20 @@ ids_np = lut_ids(a.batch, 8, a.seed)
 m = messages(a.batch, P.p, a.seed)
 ct = wl.encrypt(P, m, lwe_randomness(P, a.batch, a.seed), keys["big_key"], dev)
 torch.cuda.synchronize()
-silenzio.debug_fft_margin()  # reset (key setup ran no blind rotation, but be explicit)
+silenzio.debug_fft_margin()  # reset
 out = silenzio.pbs_batch(ct, torch.from_numpy(ids_np.astype(np.int32)).to(dev), luts, keys["fbsk"], keys["ksk"], P)
 torch.cuda.synchronize()
-frac, mx = silenzio.debug_fft_margin()
+limbs = silenzio.debug_fft_margin()
 dec = wl.decode(wl.to_host_u64(silenzio.lwe_phase_batch(out, keys["big_key"])), P.p)
+per_limb = {}
+for p, d in enumerate(limbs):
+    per_limb[f"limb{p}_shift{p * P.limb_bits}"] = {
+        "max_abs_frac": d["max_frac"], "max_abs_limb_sum": d["max_abs"],
+        "max_abs_limb_sum_log2": math.log2(d["max_abs"]) if d["max_abs"] > 0 else None,
+        "values_frac_ge_quarter": d["n_ge_quarter"], "values_frac_ge_half": d["n_ge_half"]}
 rep = {"workload": f"configs[1], batch {a.batch}, set A, P = 3 (limbs {P.limb_bits}/{P.limb_bits}/{64 - 2 * P.limb_bits})",
-       "limb_values_rounded": a.batch * P.n * 2 * P.fft_limbs * P.N,
-       "max_abs_frac": frac, "max_abs_frac_log2": math.log2(frac) if frac > 0 else None,
-       "max_abs_limb_sum": mx, "max_abs_limb_sum_log2": math.log2(mx) if mx > 0 else None,
-       "exact_rounding_margin": 0.5 / frac if frac > 0 else None,
+       "limb_values_rounded_per_limb": a.batch * P.n * 2 * P.N, "per_limb": per_limb,
+       "note": "a value at |x - round(x)| >= 1/2 is a rounding tie whose true integer the f64 result cannot tell "
+               "(a possible slip of 1 unit at that limb's weight, 2^(22 p)); >= 1/4 counts the near-ties",
        "decrypt_failures": int((dec != tabs[ids_np, m]).sum())}
 print(json.dumps(rep))
