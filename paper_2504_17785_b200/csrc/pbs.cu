@@ -18,8 +18,7 @@
 // L2 latency of the BSK stream is then hidden behind FFT arithmetic. The
 // decomposed digits' spectra are staged in shared memory (one 16 KiB array per
 // GGSW row); every transform is register resident (16 complex per thread) with
-// two shared-memory exchanges. Compile with -DSZ_BR_ACC_REG for the previous
-// variant (ACC in registers, no prefetch) for A/B measurements.
+// two shared-memory exchanges.
 #include <cmath>
 #include <mutex>
 
@@ -223,126 +222,12 @@ __device__ __forceinline__ u64 acc_init(const u64 *v, int j, int bt, int team) {
   return team ? vv : 0ull;
 }
 
-#ifdef SZ_BR_ACC_REG
-// ---- previous variant: ACC in registers (thread t of team g owns ACC_g[j] for
-// j = t + 64 m + 1024 h), BSK loaded four slots at a time in the MAC.
-template <int L, int P>
-__global__ void __launch_bounds__(128, 2) blind_rotate_kernel(BRArgs A) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  constexpr int rows = 2 * L;
-  double2 *tbuf_all = reinterpret_cast<double2 *>(smem);
-  double2 *dsm = tbuf_all + 2 * kM;
-  unsigned short *abar = reinterpret_cast<unsigned short *>(dsm + (size_t)rows * kM);
-  const int tid = threadIdx.x, team = tid >> 6, t = tid & 63;
-  double2 *tbuf = tbuf_all + team * kM;
-  u64 *accs = reinterpret_cast<u64 *>(tbuf);
-  const int n = A.n, w = A.w, blog = A.base_log;
-  for (long c = blockIdx.x; c < A.count; c += gridDim.x) {
-    const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
-    for (int i = tid; i < n; i += 128) abar[i] = (unsigned short)sz_modswitch(lwe[i], kLog2_2N);
-    const int bt = (int)sz_modswitch(lwe[n], kLog2_2N);
-    u32 id = A.lut_ids ? A.lut_ids[c] : 0u;
-    if (id >= A.num_luts) id = 0;
-    const u64 *v = A.luts + (size_t)id * kN;
-    u64 accr[16][2];
-#pragma unroll
-    for (int m = 0; m < 16; m++)
-#pragma unroll
-      for (int h = 0; h < 2; h++) accr[m][h] = acc_init(v, t + 64 * m + 1024 * h, bt, team);
-    __syncthreads();
-    for (int i = 0; i < n; i++) {
-      const int a = abar[i];
-#pragma unroll
-      for (int m = 0; m < 16; m++)
-#pragma unroll
-        for (int h = 0; h < 2; h++) accs[t + 64 * m + 1024 * h] = accr[m][h];
-      team_sync(team);
-#pragma unroll 1
-      for (int lvl = 1; lvl <= L; lvl++) {
-        double2 x[16];
-#pragma unroll
-        for (int m = 0; m < 16; m++) {
-          double dv[2];
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            const int j = t + 64 * m + 1024 * h;
-            const int src = (j - a) & (2 * kN - 1);
-            const u64 rv = accs[src & (kN - 1)];
-            const u64 rot = (src < kN) ? rv : (u64)0 - rv;
-            u64 r = sz_decomp_round(rot - accr[m][h], blog, L);
-            i64 d = 0;
-#pragma unroll
-            for (int tt = L; tt >= 1; tt--) {
-              const i64 dd = sz_decomp_next(r, blog);
-              if (tt == lvl) d = dd;
-            }
-            dv[h] = (double)d;
-          }
-          x[m] = make_double2(dv[0], dv[1]);
-        }
-        double2 *drow = dsm + (size_t)(team * L + (lvl - 1)) * kM;
-        fwd_fft<false>(x, drow, t, team);
-        team_sync(team);
-#pragma unroll
-        for (int sl = 0; sl < 16; sl++) drow[sl * 64 + t] = x[sl];
-      }
-      __syncthreads();
-      const double2 *Gi = A.fbsk + ((size_t)i * 2 + team) * rows * P * kM;
-#pragma unroll 1
-      for (int p = P - 1; p >= 0; p--) {
-        double2 y[16];
-#pragma unroll
-        for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
-#pragma unroll 1
-        for (int row = 0; row < rows; row++) {
-          const double2 *G = Gi + ((size_t)row * P + p) * kM + t;
-          const double2 *D = dsm + (size_t)row * kM + t;
-#pragma unroll
-          for (int qq = 0; qq < 4; qq++) {
-            double2 g[4], dd[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++) g[q] = __ldg(&G[(4 * qq + q) * 64]);
-#pragma unroll
-            for (int q = 0; q < 4; q++) dd[q] = D[(4 * qq + q) * 64];
-#pragma unroll
-            for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], dd[q], g[q]);
-          }
-        }
-        inv_fft<false>(y, tbuf, t, team);
-#pragma unroll
-        for (int m = 0; m < 16; m++) {
-          accr[m][0] += limb_to_torus(y[m].x, p, P, w);
-          accr[m][1] += limb_to_torus(y[m].y, p, P, w);
-        }
-      }
-      __syncthreads();
-    }
-    u64 *out = A.lwe_out + (size_t)c * (kN + 1);
-#pragma unroll
-    for (int m = 0; m < 16; m++)
-#pragma unroll
-      for (int h = 0; h < 2; h++) {
-        const int j = t + 64 * m + 1024 * h;
-        if (team == 0) {
-          if (j == 0) out[0] = accr[m][h];
-          else out[kN - j] = (u64)0 - accr[m][h];
-        } else if (j == 0) {
-          out[kN] = accr[m][h];
-        }
-      }
-    __syncthreads();
-  }
-}
-#else
 // ---- ACC in TMEM. Thread t of team g (warp 2g + t/32, TMEM lanes of its warp's
 // quadrant) keeps ACC_g[j], j = t + 64 m + 1024 h, in its own lane: u64 (m, h)
 // at columns 4m + 2h (low word) and 4m + 2h + 1 (high word), 64 columns per CTA.
 // Chunk c (16 columns) holds m = 4c .. 4c + 3.
-#ifndef SZ_TW1_TMEM
-#define SZ_TW1_TMEM 1
-#endif
 constexpr uint32_t kAccCols = 64;
-constexpr uint32_t kTmemCols = SZ_TW1_TMEM ? 128 : 64;  // ACC [0, 64) + pass-1 twiddles [64, 128)
+constexpr uint32_t kTmemCols = 128;  // ACC [0, 64) + pass-1 twiddles [64, 128)
 
 __device__ __forceinline__ void acc_load(uint32_t ta, int c, u64 (&a)[4][2]) {
   uint32_t r[16];
@@ -375,14 +260,8 @@ __device__ __forceinline__ void load_g(double2 (&g)[2][16], const double2 *G0, c
   }
 }
 
-#ifndef SZ_BR_PREFETCH
-#define SZ_BR_PREFETCH 0  // BSK rows in registers during the IFFT: 255 regs, 2 CTAs/SM (27.8k) < 3 CTAs/SM (31.7k)
-#endif
-#ifndef SZ_BR_MINB
-#define SZ_BR_MINB 3
-#endif
 template <int L, int P>
-__global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A) {
+__global__ void __launch_bounds__(128, 3) blind_rotate_kernel(BRArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ uint32_t tmem_slot;
   constexpr int rows = 2 * L;
@@ -400,7 +279,6 @@ __global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A)
   tmem_fence_after();
   const uint32_t ta = tmem_slot + ((uint32_t)(32 * wid) << 16);
   const uint32_t ta_tw = ta + kAccCols;
-#if SZ_TW1_TMEM
   // pass-1 twiddles of this thread's t, register order r (k = bitrev4(r))
 #pragma unroll
   for (int j = 0; j < 4; j++) {
@@ -412,7 +290,6 @@ __global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A)
     tmem_st16(ta_tw + 16 * j, r16);
   }
   tmem_wait_st();
-#endif
 
   // Fourier-BSK pointer of (i, output component team, row, limb p), thread offset t
   auto gptr = [&](int i, int row, int p) {
@@ -439,11 +316,6 @@ __global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A)
     }
     tmem_wait_st();
     __syncthreads();  // abar visible
-#if SZ_BR_PREFETCH
-    // operands of the first MAC (CMux 0, top limb, rows 0-1) in flight from here
-    double2 g[2][16];
-    load_g(g, gptr(0, 0, P - 1), gptr(0, 1, P - 1));
-#endif
 
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
@@ -489,7 +361,7 @@ __global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A)
           }
         }
         double2 *drow = dsm + (size_t)(team * L + (lvl - 1)) * kM;
-        fwd_fft<SZ_TW1_TMEM>(x, drow, t, team, ta_tw);  // the row's own spectrum buffer is the exchange buffer
+        fwd_fft<1>(x, drow, t, team, ta_tw);  // the row's own spectrum buffer is the exchange buffer
         team_sync(team);
 #pragma unroll
         for (int sl = 0; sl < 16; sl++) drow[sl * 64 + t] = x[sl];
@@ -501,22 +373,6 @@ __global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A)
         double2 y[16];
 #pragma unroll
         for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
-#if SZ_BR_PREFETCH
-#pragma unroll 1
-        for (int rp = 0; rp < L; rp++) {
-          if (rp > 0) load_g(g, gptr(i, 2 * rp, p), gptr(i, 2 * rp + 1, p));
-          const double2 *D0 = dsm + (size_t)(2 * rp) * kM + t;
-          const double2 *D1 = D0 + kM;
-#pragma unroll
-          for (int sl = 0; sl < 16; sl++) {
-            cmac(y[sl], D0[sl * 64], g[0][sl]);
-            cmac(y[sl], D1[sl * 64], g[1][sl]);
-          }
-        }
-        // prefetch the next MAC's operands; they arrive during this inverse FFT
-        if (p > 0) load_g(g, gptr(i, 0, p - 1), gptr(i, 1, p - 1));
-        else if (i + 1 < n) load_g(g, gptr(i + 1, 0, P - 1), gptr(i + 1, 1, P - 1));
-#else
 #pragma unroll 1
         for (int row = 0; row < rows; row++) {
           const double2 *G = gptr(i, row, p);
@@ -532,8 +388,7 @@ __global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A)
             for (int q = 0; q < 4; q++) cmac(y[4 * qq + q], dd[q], gg[q]);
           }
         }
-#endif
-        inv_fft<SZ_TW1_TMEM>(y, tbuf, t, team, ta_tw);
+        inv_fft<1>(y, tbuf, t, team, ta_tw);
 #pragma unroll
         for (int cc = 0; cc < 4; cc++) {
           u64 a4[4][2];
@@ -574,7 +429,6 @@ __global__ void __launch_bounds__(128, SZ_BR_MINB) blind_rotate_kernel(BRArgs A)
   __syncthreads();
   if (wid == 0) tmem_dealloc(tmem_slot, kTmemCols);
 }
-#endif
 
 // --------------------------------------------------------- BSK -> Fourier
 struct B2FArgs {
@@ -633,7 +487,6 @@ static int plan_blind_rotate(const silenzio_params *P, BRPlan *plan) {
   SZ_CUDA_OK(cudaGetDevice(&dev));
   SZ_CUDA_OK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   SZ_CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
-#ifndef SZ_BR_ACC_REG
   // The occupancy API under-reports residency for this (TMEM-allocating) kernel
   // (1 CTA/SM where ncu's "Block Limit" registers/shared memory give 2): size
   // the wave from registers, shared memory and TMEM columns instead.
@@ -649,7 +502,6 @@ static int plan_blind_rotate(const silenzio_params *P, BRPlan *plan) {
     if (per_sm > by_tmem) per_sm = by_tmem;
     if (per_sm < 1) per_sm = 1;
   }
-#endif
   if (per_sm < 1) return SILENZIO_ERR_UNSUPPORTED;
   plan->kern = kern;
   plan->smem = smem;

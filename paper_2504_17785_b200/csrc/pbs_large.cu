@@ -10,7 +10,7 @@
 // stays in shared memory. The (k+1)l = 4 digit spectra of a CMux are
 // thread-private (each thread's MAC reads exactly the slots its own forward
 // pass produced), so they live in this thread's lane of tensor memory (4 x 64
-// columns per lane quadrant, SZ_SETC_TMEM; the SZ_SETC_TMEM = 0 build keeps
+// columns per lane quadrant, 1; the 1 = 0 build keeps
 // them in per-thread local memory), with no synchronisation and no workspace.
 #include <cmath>
 #include <mutex>
@@ -166,11 +166,6 @@ __device__ __forceinline__ u64 limb_to_torus_L(double x, int p, int P, int w) {
   return f64_to_torus_L(x);
 }
 
-#ifndef SZ_SETC_TMEM
-#define SZ_SETC_TMEM 1  // digit spectra in TMEM instead of (L2-backed) local memory
-#endif
-
-
 struct BRLArgs {
   const u64 *lwe_small;
   const u32 *lut_ids;
@@ -186,16 +181,6 @@ __host__ __device__ constexpr size_t brl_smem_bytes(int n) {
   return 2 * kNL * sizeof(u64) + kML * sizeof(double2) + ((size_t)n * 2 + 15) / 16 * 16;
 }
 
-
-#ifndef SZ_L2PF
-#define SZ_L2PF 1  // bulk L2 prefetch of the next MAC round's Fourier-BSK rows (set C: +1.7 %)
-#endif
-#ifndef SZ_L2PF_AHEAD
-#define SZ_L2PF_AHEAD 1  // MAC rounds ahead the set-C prefetch runs
-#endif
-#ifndef SZ_L2PF_B
-#define SZ_L2PF_B 0  // the same on the set-B cluster kernel: measured 3-6 % slower, off
-#endif
 // one thread asks the copy engine to pull a contiguous chunk into L2 (no
 // registers, no completion tracking): the next round's BSK rows arrive while
 // the current round computes, so the MAC's loads hit L2 instead of HBM
@@ -215,7 +200,7 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
   // thread-private digit spectra: in tensor memory when they fit (rows <= 4:
   // threads t and t + 128 share a lane (warps w, w + 4), columns [0, 256) and
   // [256, 512); row r, slot sl at column 64 r + 4 sl), else in local memory
-  constexpr bool kTm = SZ_SETC_TMEM && rows <= 4;
+  constexpr bool kTm = rows <= 4;
   __shared__ uint32_t tmem_slot;
   const int wid = t >> 5;
   if constexpr (kTm) {
@@ -241,18 +226,18 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
     __syncthreads();
     // rows of (i, o, p) for this CTA: rows chunks of kML double2, stride P kML
     auto prefetch_round = [&](int i, int o, int p) {
-      if (SZ_L2PF && t == 0 && i < n)
+      if (t == 0 && i < n)
         for (int row = 0; row < rows; row++)
           l2_prefetch_bulk(A.fbsk + (((size_t)i * 2 + o) * rows + row) * P * kML + (size_t)p * kML,
                            kML * sizeof(double2));
     };
-    // MAC round k of CMux i (k = o P + P - 1 - p, 2P rounds) -> prefetch k + SZ_L2PF_AHEAD
+    // MAC round k of CMux i (k = o P + P - 1 - p, 2P rounds) -> prefetch k + 1
     auto prefetch_ahead = [&](int i, int k) {
       i += k / (2 * P);
       k %= 2 * P;
       prefetch_round(i, k / P, P - 1 - k % P);
     };
-    for (int k = 0; k < SZ_L2PF_AHEAD; k++) prefetch_ahead(0, k);
+    prefetch_ahead(0, 0);
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
       // -------- forward: every (component r, level lvl) digit polynomial
@@ -306,7 +291,7 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
         u64 *acco = acc + o * kNL;
 #pragma unroll 1
         for (int p = P - 1; p >= 0; p--) {
-          prefetch_ahead(i, o * P + (P - 1 - p) + SZ_L2PF_AHEAD);
+          prefetch_ahead(i, o * P + (P - 1 - p) + 1);
           double2 y[16];
 #pragma unroll
           for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
@@ -458,7 +443,6 @@ int launch_bsk_to_fourier_large(const u64 *bsk, void *fbsk, const silenzio_param
   SZ_LAUNCH_OK();
   return SILENZIO_OK;
 }
-
 
 // =====================================================================
 // N = 32768 (parameter set B, BASELINE configs[4] 8-bit stage).
@@ -741,9 +725,6 @@ __global__ void __launch_bounds__(256) bsk_to_fourier_huge_kernel(B2FHArgs A) {
 //    buffer; inverse, CTA q stores its block output at pp into the owner of pp,
 //    which combines the four blocks, rounds and updates its ACC slice.
 // Cluster barriers order the exchanges (two per forward row and per (o, p)).
-#ifndef SZ_SETB_CLUSTER
-#define SZ_SETB_CLUSTER 1  // 0: the global-memory blind_rotate_huge_kernel for every set-B shape
-#endif
 constexpr int kClQ = 4;  // CTAs per ciphertext = radix-4 blocks
 __host__ __device__ constexpr size_t brc_acc_bytes() { return 2 * 2 * 4 * 1024 * sizeof(u64); }
 __host__ __device__ constexpr size_t brc_smem_bytes(int n) {
@@ -751,9 +732,6 @@ __host__ __device__ constexpr size_t brc_smem_bytes(int n) {
 }
 __device__ __forceinline__ int brc_aidx(int comp, int h, int mp, int loc) { return ((comp * 2 + h) * 4 + mp) * 1024 + loc; }
 
-#ifndef SZ_SETB_ASYNCX
-#define SZ_SETB_ASYNCX 1  // exchanges by st.async + mbarriers (point-to-point) instead of cluster barriers
-#endif
 // ---- cluster exchange primitives (shared::cluster addresses are 32-bit)
 __device__ __forceinline__ uint32_t cl_mapa(uint32_t saddr, int rank) {
   uint32_t r;
@@ -766,13 +744,6 @@ __device__ __forceinline__ void cl_mbar_init(uint32_t mbar, uint32_t count) {
 // arm this CTA's receive barrier for `bytes` of incoming st.async data (one arrival)
 __device__ __forceinline__ void cl_mbar_expect(uint32_t mbar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes) : "memory");
-}
-#ifndef SZ_SETB_RELFENCE
-#define SZ_SETB_RELFENCE 1  // one release fence + relaxed arrives (0: a release-arrive per remote barrier)
-#endif
-// release-arrive on a barrier of another CTA of the cluster
-__device__ __forceinline__ void cl_mbar_arrive_remote(uint32_t rmbar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rmbar) : "memory");
 }
 // relaxed arrive: ordering comes from a preceding fence.release.cluster (ptxas
 // emits the full MEMBAR.GPU + ERRBAR sequence once per fence instead of once per
@@ -810,20 +781,14 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
   const int q = (int)cl.block_rank();
   const int n = A.n, w = A.w, blog = A.base_log;
   // remote (distributed shared memory) addresses: one mapa per access
-#if SZ_DBG_LOCAL
-  auto racc = [&](int rank, int idx) -> const u64 & { (void)rank; return acc[idx]; };
-  auto rbuf = [&](int rank, int idx) -> double2 & { (void)rank; return buf[idx]; };
-#else
   auto racc = [&](int rank, int idx) -> const u64 & { return *cl.map_shared_rank(acc + idx, rank); };
-  auto rbuf = [&](int rank, int idx) -> double2 & { return *cl.map_shared_rank(buf + idx, rank); };
-#endif
   __shared__ uint32_t tmem_slot;
   if (wid == 0) tmem_alloc(&tmem_slot, 512);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
   const uint32_t ta_spec = tmem_slot + ((uint32_t)(32 * (wid & 3)) << 16) + 256 * (wid >> 2);
-  // exchange rounds (SZ_SETB_ASYNCX): every round fills each CTA's buffer with
+  // exchange rounds: every round fills each CTA's buffer with
   // 4 x 16 KiB from the 4 senders. full = this CTA's receive barrier (armed
   // with 64 KiB per round); freeb = counts the 4 receivers that released their
   // buffer for the next round (this CTA sends only after all 4 did).
@@ -834,24 +799,19 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
   auto release_buf = [&]() {  // after a __syncthreads: this CTA is done with its buffer
     if (t == 0) {
       cl_mbar_expect(full, 4 * 1024 * sizeof(double2));
-      if (SZ_SETB_RELFENCE) {
-        cl_fence_release();
+      // one release fence, then relaxed remote arrivals (a release-arrive per
+      // remote barrier costs a MEMBAR + ERRBAR each: 4 % slower)
+      cl_fence_release();
 #pragma unroll
-        for (int r = 0; r < kClQ; r++) cl_mbar_arrive_remote_relaxed(cl_mapa(freeb, r));
-      } else {
-#pragma unroll
-        for (int r = 0; r < kClQ; r++) cl_mbar_arrive_remote(cl_mapa(freeb, r));
-      }
+      for (int r = 0; r < kClQ; r++) cl_mbar_arrive_remote_relaxed(cl_mapa(freeb, r));
     }
   };
-  if (SZ_SETB_ASYNCX) {
-    if (t == 0) {
-      cl_mbar_init(full, 1);
-      cl_mbar_init(freeb, kClQ);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    cl.sync();
+  if (t == 0) {
+    cl_mbar_init(full, 1);
+    cl_mbar_init(freeb, kClQ);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  cl.sync();
   const long ncl = gridDim.x / kClQ;
   for (long c = blockIdx.x / kClQ; c < A.count; c += ncl) {
     const u64 *lwe = A.lwe_small + (size_t)c * (n + 1);
@@ -869,14 +829,6 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
       acc[brc_aidx(1, h, mp, loc)] = (idx < kNH) ? v[idx] : (u64)0 - v[idx - kNH];
     }
     __syncthreads();
-    // rows of (i, o, p) for this CTA's block q: rows chunks of kML double2
-    auto prefetch_round = [&](int i, int o, int p) {
-      if (SZ_L2PF_B && t == 0 && i < n)
-        for (int row = 0; row < rows; row++)
-          l2_prefetch_bulk(A.fbsk + (((((size_t)i * 2 + o) * rows + row) * P + p) * 4 + q) * kML,
-                           kML * sizeof(double2));
-    };
-    prefetch_round(0, 0, P - 1);
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
       // -------- forward: (r, lvl) digit polynomial -> radix-4 inputs -> block FFT
@@ -884,13 +836,10 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
       for (int r = 0; r < 2; r++) {
 #pragma unroll 1
         for (int lvl = 1; lvl <= L; lvl++) {
-          if (SZ_SETB_ASYNCX) {
-            __syncthreads();  // this CTA's previous use of its buffer (FFT / combination) is over
-            release_buf();
-            cl_mbar_wait_acq(freeb, xround & 1);  // all 4 buffers free, all ACC slices final (release/acquire)
-          } else {
-            cl.sync();  // every buffer is free, every ACC update of the previous CMux is done
-          }
+          __syncthreads();  // this CTA's previous use of its buffer (FFT / combination) is over
+          release_buf();
+          cl_mbar_wait_acq(freeb, xround & 1);  // all 4 buffers free, all ACC slices final (release/acquire)
+
 #pragma unroll 1
           for (int mm = 0; mm < 4; mm++) {
             const int loc = t + 256 * mm, pp = 1024 * q + loc;
@@ -923,16 +872,12 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
 #pragma unroll
               for (int mp = 0; mp < 4; mp++) sacc = cadd(sacc, cmul(vv[mp], c_CH[mp * 4 + qq]));
               const double2 xv = cmul(sacc, g_FH[qq * 4096 + pp]);
-              if (SZ_SETB_ASYNCX) cl_st_async(cl_mapa(buf_s + pp * 16, qq), xv, cl_mapa(full, qq));
-              else rbuf(qq, pp) = xv;
+              cl_st_async(cl_mapa(buf_s + pp * 16, qq), xv, cl_mapa(full, qq));
             }
           }
-          if (SZ_SETB_ASYNCX) {
-            cl_mbar_wait_acq(full, xround & 1);  // block inputs delivered
-            xround++;
-          } else {
-            cl.sync();  // block inputs delivered
-          }
+          cl_mbar_wait_acq(full, xround & 1);  // block inputs delivered
+          xround++;
+
           double2 x[16];
 #pragma unroll
           for (int m = 0; m < 16; m++) x[m] = buf[t + 256 * m];
@@ -952,9 +897,6 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
       for (int o = 0; o < 2; o++) {
 #pragma unroll 1
         for (int p = P - 1; p >= 0; p--) {
-          if (p > 0) prefetch_round(i, o, p - 1);
-          else if (o == 0) prefetch_round(i, 1, P - 1);
-          else prefetch_round(i + 1, 0, P - 1);
           double2 y[16];
 #pragma unroll
           for (int sl = 0; sl < 16; sl++) y[sl] = make_double2(0.0, 0.0);
@@ -978,26 +920,17 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
             }
           }
           inv_fft_L(y, buf, t);
-          if (SZ_SETB_ASYNCX) {
-            __syncthreads();  // this CTA's IFFT is done with its buffer
-            release_buf();
-            cl_mbar_wait_acq(freeb, xround & 1);
+          __syncthreads();  // this CTA's IFFT is done with its buffer
+          release_buf();
+          cl_mbar_wait_acq(freeb, xround & 1);
 #pragma unroll
-            for (int m = 0; m < 16; m++) {
-              const int pp = t + 256 * m;
-              cl_st_async(cl_mapa(buf_s + (q * 1024 + (pp & 1023)) * 16, pp >> 10), y[m], cl_mapa(full, pp >> 10));
-            }
-            cl_mbar_wait_acq(full, xround & 1);  // block outputs delivered to the owners
-            xround++;
-          } else {
-            cl.sync();  // every block IFFT is done with its buffer
-#pragma unroll
-            for (int m = 0; m < 16; m++) {
-              const int pp = t + 256 * m;
-              rbuf(pp >> 10, q * 1024 + (pp & 1023)) = y[m];
-            }
-            cl.sync();  // block outputs delivered to the owners
+          for (int m = 0; m < 16; m++) {
+            const int pp = t + 256 * m;
+            cl_st_async(cl_mapa(buf_s + (q * 1024 + (pp & 1023)) * 16, pp >> 10), y[m], cl_mapa(full, pp >> 10));
           }
+          cl_mbar_wait_acq(full, xround & 1);  // block outputs delivered to the owners
+          xround++;
+
 #pragma unroll 1
           for (int mm = 0; mm < 4; mm++) {
             const int loc = t + 256 * mm, pp = 1024 * q + loc;
@@ -1039,7 +972,7 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
 }
 
 static bool cluster_path(const silenzio_params *P) {
-  return SZ_SETB_CLUSTER && P->pbs_level <= 2 && P->fft_limbs == 3 && brc_smem_bytes((int)P->lwe_dim) <= 227 * 1024;
+  return P->pbs_level <= 2 && P->fft_limbs == 3 && brc_smem_bytes((int)P->lwe_dim) <= 227 * 1024;
 }
 
 // max co-resident clusters for (device, kernel, dynamic smem), cached (the
