@@ -351,6 +351,11 @@ int silenzio_debug_fft_margin(double *out);
  * phases: publish, digits, forward FFT, spectra exchange, stage wait, MAC,
  * inverse FFT, recombination); resets them. Release builds: UNSUPPORTED. */
 int silenzio_debug_phase_times(unsigned long long *out);
+/* The same for the set-B (N = 32768) cluster kernel: out[12] cycles per phase
+ * of CTA 0 thread 0 (forward free-wait, digits + radix-4 + sends, forward
+ * full-wait, block FFT, MAC, block IFFT, inverse free-wait, sends, inverse
+ * full-wait, combine + ACC update). Release builds: UNSUPPORTED. */
+int silenzio_debug_phase_times_b(unsigned long long *out);
 
 #ifdef __cplusplus
 }

@@ -19,6 +19,7 @@
 #include <cooperative_groups.h>
 
 #include "fft.cuh"
+#include "limbs.cuh"
 #include "tmem.cuh"
 
 namespace sz {
@@ -162,7 +163,10 @@ __device__ __forceinline__ u64 f64_to_torus_L(double x) {
 }
 
 __device__ __forceinline__ u64 limb_to_torus_L(double x, int p, int P, int w) {
-  if (P == 3 || p > 0) return (u64)__double2ll_rn(x) << (p * w);
+  // P = 3: |x| < 2^51 (R20), rounded on the FP64 pipe (1.5 * 2^52 trick)
+  // instead of a 64-bit F2I conversion
+  if (P == 3) return rint_small(x) << (p * w);
+  if (p > 0) return (u64)__double2ll_rn(x) << (p * w);
   return f64_to_torus_L(x);
 }
 
@@ -767,6 +771,27 @@ __device__ __forceinline__ void cl_st_async(uint32_t raddr, double2 v, uint32_t 
                : "memory");
 }
 
+#ifndef SZ_PHASE_TIMING
+#define SZ_PHASE_TIMING 0  // 1: debug build accumulating clock64 per CMux phase (CTA 0, thread 0)
+#endif
+#if SZ_PHASE_TIMING
+__device__ unsigned long long g_phase_b[12];
+#define SZB_PT_INIT long long szb_prev = clock64();
+#define SZB_PT(k)                                                              \
+  do {                                                                         \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                 \
+      const long long now = clock64();                                         \
+      g_phase_b[k] += (unsigned long long)(now - szb_prev);                    \
+      szb_prev = now;                                                          \
+    }                                                                          \
+  } while (0)
+#else
+#define SZB_PT_INIT
+#define SZB_PT(k) \
+  do {            \
+  } while (0)
+#endif
+
 template <int L, int P>
 __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rotate_cluster_kernel(BRHArgs A) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -829,6 +854,7 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
       acc[brc_aidx(1, h, mp, loc)] = (idx < kNH) ? v[idx] : (u64)0 - v[idx - kNH];
     }
     __syncthreads();
+    SZB_PT_INIT
     for (int i = 0; i < n; i++) {
       const int a = abar[i];
       // -------- forward: (r, lvl) digit polynomial -> radix-4 inputs -> block FFT
@@ -839,6 +865,7 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
           __syncthreads();  // this CTA's previous use of its buffer (FFT / combination) is over
           release_buf();
           cl_mbar_wait_acq(freeb, xround & 1);  // all 4 buffers free, all ACC slices final (release/acquire)
+          SZB_PT(0);
 
 #pragma unroll 1
           for (int mm = 0; mm < 4; mm++) {
@@ -875,8 +902,10 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
               cl_st_async(cl_mapa(buf_s + pp * 16, qq), xv, cl_mapa(full, qq));
             }
           }
+          SZB_PT(1);
           cl_mbar_wait_acq(full, xround & 1);  // block inputs delivered
           xround++;
+          SZB_PT(2);
 
           double2 x[16];
 #pragma unroll
@@ -889,6 +918,7 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
             pack4(&x[4 * jj], r16);
             tmem_st16(ta_spec + 64 * row + 16 * jj, r16);
           }
+          SZB_PT(3);
         }
       }
       tmem_wait_st();
@@ -919,17 +949,22 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
               }
             }
           }
+          SZB_PT(4);
           inv_fft_L(y, buf, t);
+          SZB_PT(5);
           __syncthreads();  // this CTA's IFFT is done with its buffer
           release_buf();
           cl_mbar_wait_acq(freeb, xround & 1);
+          SZB_PT(6);
 #pragma unroll
           for (int m = 0; m < 16; m++) {
             const int pp = t + 256 * m;
             cl_st_async(cl_mapa(buf_s + (q * 1024 + (pp & 1023)) * 16, pp >> 10), y[m], cl_mapa(full, pp >> 10));
           }
+          SZB_PT(7);
           cl_mbar_wait_acq(full, xround & 1);  // block outputs delivered to the owners
           xround++;
+          SZB_PT(8);
 
 #pragma unroll 1
           for (int mm = 0; mm < 4; mm++) {
@@ -946,6 +981,7 @@ __global__ void __cluster_dims__(kClQ, 1, 1) __launch_bounds__(256, 1) blind_rot
               acc[brc_aidx(o, 1, mp, loc)] += limb_to_torus_L(sacc.y, p, P, w);
             }
           }
+          SZB_PT(9);
         }
       }
     }
@@ -1187,3 +1223,20 @@ int launch_glwe_body_huge(const u64 *Amask, size_t a_stride, const u64 *key, con
 }
 
 }  // namespace sz
+
+// SZ_PHASE_TIMING debug builds: clock64 cycles per phase of the set-B cluster
+// kernel's CMux loop (CTA 0, thread 0): 0 forward release/free-wait, 1 digits +
+// radix-4 + sends, 2 forward full-wait, 3 block FFT + TMEM store, 4 MAC,
+// 5 block IFFT, 6 inverse release/free-wait, 7 sends, 8 inverse full-wait,
+// 9 combine + rounding + ACC update; read and reset
+extern "C" int silenzio_debug_phase_times_b(unsigned long long *out /* [12] */) {
+#if SZ_PHASE_TIMING
+  unsigned long long z[12] = {0};
+  SZ_CUDA_OK(cudaMemcpyFromSymbol(out, sz::g_phase_b, sizeof(z)));
+  SZ_CUDA_OK(cudaMemcpyToSymbol(sz::g_phase_b, z, sizeof(z)));
+  return SILENZIO_OK;
+#else
+  (void)out;
+  return SILENZIO_ERR_UNSUPPORTED;
+#endif
+}

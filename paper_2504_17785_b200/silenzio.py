@@ -80,6 +80,7 @@ def load():
         "silenzio_pbs_trace_end": ([I, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_long),
         "silenzio_debug_fft_margin": ([V], I),
         "silenzio_debug_phase_times": ([V], I),
+        "silenzio_debug_phase_times_b": ([V], I),
     }
     for name, (args, res) in sigs.items():
         fn = getattr(L, name)
@@ -103,7 +104,7 @@ def exported_symbols():
         "silenzio_shift2msbs_workspace_bytes", "silenzio_shift2msbs_pm",
         "silenzio_train_workspace_bytes", "silenzio_channel16", "silenzio_rns_sign3", "silenzio_relu_cap",
         "silenzio_relu_mask", "silenzio_weight_update", "silenzio_pbs_trace_begin", "silenzio_pbs_trace_end",
-        "silenzio_debug_fft_margin", "silenzio_debug_phase_times",
+        "silenzio_debug_fft_margin", "silenzio_debug_phase_times", "silenzio_debug_phase_times_b",
     ]
 
 
