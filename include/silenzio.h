@@ -349,7 +349,9 @@ int silenzio_debug_fft_margin(double *out);
 /* Debug builds only (-DSZ_PHASE_TIMING=1, tools/phase_times.py): clock64 cycles
  * accumulated per phase of the set-A CMux loop, out[warp][phase] (8 x 8, CTA 0,
  * phases: publish, digits, forward FFT, spectra exchange, stage wait, MAC,
- * inverse FFT, recombination); resets them. Release builds: UNSUPPORTED. */
+ * inverse FFT, recombination; for batches the latency kernel takes,
+ * tools/phase_times_lat.py names its phases); resets them. Release builds:
+ * UNSUPPORTED. */
 int silenzio_debug_phase_times(unsigned long long *out);
 /* The same for the set-B (N = 32768) cluster kernel: out[12] cycles per phase
  * of CTA 0 thread 0 (forward free-wait, digits + radix-4 + sends, forward

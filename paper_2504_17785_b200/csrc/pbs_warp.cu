@@ -424,7 +424,7 @@ __device__ unsigned long long g_phase[8][8];
     }                                                                   \
   } while (0)
 #else
-#define SZ_PT_INIT
+#define SZ_PT_INIT long long sz_pt_prev = 0;
 #define SZ_PT(k) \
   do {           \
   } while (0)
@@ -680,7 +680,10 @@ __host__ __device__ constexpr size_t lat_smem_bytes(int n) {
 // phase F of one CMux for GLWE component r (warps 0, 1)
 template <int P>
 __device__ __forceinline__ void lat_forward(ulonglong2 *ac, const ulonglong2 *contrib, double2 *dhat_r,
-                                            double2 *xbuf, int a, bool add, int lane, u64 half_q, int blog) {
+                                            double2 *xbuf, int a, bool add, int lane, u64 half_q, int blog,
+                                            long long &sz_pt_prev, int wid) {
+  (void)sz_pt_prev;
+  (void)wid;
   if (add) {  // ACC_r += the limb contributions of the previous CMux
 #pragma unroll 4
     for (int s = lane; s < kM; s += 32) {
@@ -695,6 +698,7 @@ __device__ __forceinline__ void lat_forward(ulonglong2 *ac, const ulonglong2 *co
     }
     __syncwarp();
   }
+  SZ_PT(0);
   // digits of X^a ACC_r - ACC_r (a4.1-a4.2), as in blind_rotate_warp_kernel
   double2 x[32];
 #pragma unroll
@@ -709,9 +713,12 @@ __device__ __forceinline__ void lat_forward(ulonglong2 *ac, const ulonglong2 *co
     x[m] = make_double2((double)((i64)(r0 - own.x + half_q) >> (64 - blog)),
                         (double)((i64)(r1 - own.y + half_q) >> (64 - blog)));
   }
+  SZ_PT(1);
   fwd_fft32(x, xbuf, lane);
+  SZ_PT(2);
 #pragma unroll
   for (int k2 = 0; k2 < 32; k2++) dhat_r[32 * k2 + lane] = x[k2];
+  SZ_PT(3);
 }
 
 template <int P>
@@ -743,10 +750,13 @@ __global__ void __launch_bounds__(kLatThreads, 1) blind_rotate_lat_kernel(Args A
           ac[s] = make_ulonglong2(acc_init(v, s, bt, r), acc_init(v, s + 1024, bt, r));
       }
       __syncthreads();  // abar complete
+      SZ_PT_INIT
       for (int i = 0; i < n; i++) {
-        lat_forward<P>(ac, contrib, dhat + r * kM, xbuf, abar[i], i > 0, lane, half_q, blog);
+        lat_forward<P>(ac, contrib, dhat + r * kM, xbuf, abar[i], i > 0, lane, half_q, blog, sz_pt_prev, wid);
         __syncthreads();  // D^ published (and the previous contributions consumed)
+        SZ_PT(4);
         __syncthreads();  // contributions of CMux i written
+        SZ_PT(5);
       }
       // ACC += the last contributions, then sample extraction (a5)
       u64 *out = A.lwe_out + (size_t)c * (kN + 1);
@@ -783,8 +793,10 @@ __global__ void __launch_bounds__(kLatThreads, 1) blind_rotate_lat_kernel(Args A
       };
       if (active) load_g(0);
       __syncthreads();  // abar complete
+      SZ_PT_INIT
       for (int i = 0; i < n; i++) {
         __syncthreads();  // D^ published
+        SZ_PT(0);
         if (active) {
           double2 (&y)[32] = g0;  // the MAC output overwrites the BSK row-0 registers
 #pragma unroll
@@ -794,9 +806,11 @@ __global__ void __launch_bounds__(kLatThreads, 1) blind_rotate_lat_kernel(Args A
             cmac(acc, dhat[kM + 32 * k2 + lane], g1[k2]);
             y[k2] = acc;
           }
+          SZ_PT(1);
           ulonglong2 *contrib = reinterpret_cast<ulonglong2 *>(xbuf);
           if constexpr (P == 3) {
             inv_fft32<false>(y, xbuf, lane);
+            SZ_PT(2);
             __syncwarp();  // the transposition's readers of xbuf are done
             const u64 off = (p == 0) ? limb_off : 0ull;  // all limbs' magic share, removed once
 #pragma unroll
@@ -813,10 +827,13 @@ __global__ void __launch_bounds__(kLatThreads, 1) blind_rotate_lat_kernel(Args A
               contrib[lane + 32 * m] =
                   make_ulonglong2(limb_to_torus(y[m].x, p, P, w), limb_to_torus(y[m].y, p, P, w));
           }
+          SZ_PT(3);
           // the next BSK slice: its loads land while phase F of CMux i + 1 runs
           if (i + 1 < n) load_g(i + 1);
+          SZ_PT(4);
         }
         __syncthreads();  // contributions written
+        SZ_PT(5);
       }
     }
     __syncthreads();  // abar / ACC / contributions reuse by the next ciphertext
