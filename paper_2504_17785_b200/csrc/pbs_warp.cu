@@ -409,6 +409,23 @@ __device__ __forceinline__ void acc_st(uint32_t ta, int cc, const u64 (&a)[kCQ][
 
 constexpr u64 kMagicBits = 0x4338000000000000ull;  // bits of 1.5 * 2^52
 
+// Throughput layout: cycles the body warp of a ciphertext waits after the
+// spectra exchange of every CMux, so that the two warps of a scheduler (the
+// two GLWE components of one ciphertext) stop running the same phase at the
+// same time: one warp's transpositions, MAC (shared-memory bound) and limb
+// recombination (integer / TMEM work) then overlap the other's FP64
+// butterflies. The wait costs both warps ~SZ_PAIR_SKEW idle cycles per CMux
+// (the mask warp meets it again at the next exchange barrier) and still nets
+// +5.9 % (profiles/r02_ab_pair_skew.txt; 0 disables).
+#ifndef SZ_PAIR_SKEW
+#define SZ_PAIR_SKEW 800
+#endif
+__device__ __forceinline__ void spin_cycles(int c) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < c) {
+  }
+}
+
 #ifndef SZ_PHASE_TIMING
 #define SZ_PHASE_TIMING 0  // 1: debug build accumulating clock64 per CMux phase (CTA 0, lane 0 of each warp)
 #endif
@@ -556,6 +573,7 @@ __global__ void __launch_bounds__(Lay<SMALL>::threads, 1) blind_rotate_warp_kern
         asm volatile("bar.sync %0, %1;" ::"r"(1 + cs), "r"(64) : "memory");  // D^_0 and D^_1 written
         tmem_fence_after();
       }
+      if (!SMALL && SZ_PAIR_SKEW > 0 && g == 1) spin_cycles(SZ_PAIR_SKEW);
       SZ_PT(3);
       // ---------------- per limb: MAC with the staged BSK, inverse FFT, exact ACC update
 #pragma unroll 1
@@ -563,7 +581,7 @@ __global__ void __launch_bounds__(Lay<SMALL>::threads, 1) blind_rotate_warp_kern
         mbar_wait(mbar, round & 1);
         round++;
         SZ_PT(4);
-        double2 y[32];
+        double2 (&y)[32] = x;  // the MAC output overwrites the digit-spectrum registers (now in TMEM / smem)
         const double2 *G0 = gbuf + (size_t)(2 * g) * kM + lane;  // [o = g][row 0]
         const double2 *G1 = G0 + kM;                             // [o = g][row 1]
         if constexpr (SMALL) {
