@@ -129,6 +129,39 @@ int silenzio_pbs_batch(const uint64_t *lwe_in, const uint32_t *lut_ids, const ui
                        uint64_t *lwe_out, size_t count, const silenzio_params *params,
                        void *workspace, void *stream);
 
+/* KSK byte planes, a once-per-key conversion like silenzio_bsk_to_fourier
+ * (SURVEY.md §8(a) a1): the keyswitching key split into its 8 byte planes in
+ * the tensor-core operand layout, silenzio_ksk_planes_bytes()
+ * device bytes (63 MB at set A; 0 when the parameters do not admit the
+ * tensor-core keyswitch, in which case silenzio_ksk_to_planes returns
+ * SILENZIO_ERR_UNSUPPORTED). planes: 16-byte aligned. */
+size_t silenzio_ksk_planes_bytes(const silenzio_params *params);
+int silenzio_ksk_to_planes(const uint64_t *ksk, void *planes, const silenzio_params *params,
+                           void *stream);
+
+/* PBS of linear combinations, the gadgets' "linear op, then lookup" step as
+ * one call (SURVEY.md §8(a) a0 fused into a1):
+ *   x_i   = sum_{t<terms} coef[i][t] * in[idx[i][t]] + (0,...,0,cst[i])   mod 2^64
+ *   out_i = PBS(x_i; luts[lut_ids[i]])
+ * The combination is formed inside the keyswitch's digit-decomposition kernel
+ * and never written to memory; the keyswitch uses the prepared byte planes
+ * (silenzio_ksk_to_planes). Bit-identical to silenzio_lwe_linear_batch followed
+ * by silenzio_pbs_batch.
+ *  in        [*][kN+1] big-key LWE; idx [count][terms] u32 rows of `in`,
+ *            coef [count][terms] i64, cst [count] u64 or NULL. idx = NULL (then
+ *            coef and cst must be NULL too): x_i = in[i], a plain PBS.
+ *  lut_ids, luts, num_luts, fourier_bsk, lwe_out as in silenzio_pbs_batch;
+ *            lwe_out may alias `in` (every input is consumed by the keyswitch
+ *            before the blind rotation writes).
+ *  workspace >= silenzio_pbs_linear_workspace_bytes(params, count), 16-byte aligned.
+ * SILENZIO_ERR_UNSUPPORTED when the parameters have no tensor-core keyswitch. */
+size_t silenzio_pbs_linear_workspace_bytes(const silenzio_params *params, size_t count);
+int silenzio_pbs_linear_batch(const uint64_t *in, const uint32_t *idx, const int64_t *coef,
+                              const uint64_t *cst, uint32_t terms, const uint32_t *lut_ids,
+                              const uint64_t *luts, uint32_t num_luts, const void *fourier_bsk,
+                              const void *ksk_planes, uint64_t *lwe_out, size_t count,
+                              const silenzio_params *params, void *workspace, void *stream);
+
 /* Blind rotation + sample extraction only (MS -> BR -> SE) of small-key
  * inputs [count][n+1]; output [count][kN+1]. Used to check the stages
  * separately against the oracle, for the literal MS->BR->SE->KS order and for

@@ -24,6 +24,11 @@ long blind_rotate_huge_wave(const silenzio_params *);
 int launch_keyswitch(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, cudaStream_t);
 size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log, size_t count);
 int launch_keyswitch_tc(const u64 *, const u64 *, u64 *, size_t, int, int, int, int, void *, cudaStream_t);
+size_t keyswitch_tc_planes_bytes(int in_dim, int n, int level, int base_log);
+size_t keyswitch_tc_scratch_bytes(int in_dim, int level, size_t count);
+int launch_ks_planes(const u64 *, void *, int, int, int, int, cudaStream_t);
+int launch_keyswitch_tc_planes(const u64 *, const u32 *, const i64 *, const u64 *, int, const void *, void *, u64 *,
+                               size_t, int, int, int, int, cudaStream_t);
 int launch_lwe_encrypt(const u64 *, const i64 *, const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_lwe_phase(const u64 *, const u64 *, int, size_t, u64 *, cudaStream_t);
 int launch_bsk_generate(const u64 *, const u64 *, const u64 *, const i64 *, u64 *, int, int, int, int, int,
@@ -214,6 +219,63 @@ int silenzio_pbs_batch(const uint64_t *in, const uint32_t *lut_ids, const uint64
   {
     SZ_RANGE("pbs.keyswitch");
     if ((st = run_keyswitch(in, ksk, small, count, P, ks_ws, sz_stream(stream)))) return st;
+  }
+  return silenzio_blind_rotate_batch(small, lut_ids, luts, num_luts, fbsk, out, count, P, br_ws, stream);
+}
+
+size_t silenzio_ksk_planes_bytes(const silenzio_params *P) {
+  if (check_params(P) != SILENZIO_OK || check_ks_params(P) != SILENZIO_OK) return 0;
+  return round_up(keyswitch_tc_planes_bytes((int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_level, (int)P->ks_base_log),
+                  256);
+}
+
+int silenzio_ksk_to_planes(const uint64_t *ksk, void *planes, const silenzio_params *P, void *stream) {
+  SZ_RANGE("ksk_to_planes");
+  int st = check_params(P);
+  if (st) return st;
+  if ((st = check_ks_params(P))) return st;
+  if (!ksk || !planes) return SILENZIO_ERR_NULL_POINTER;
+  if (!sz_aligned(ksk, 8) || !sz_aligned16(planes)) return SILENZIO_ERR_MISALIGNED;
+  if (silenzio_ksk_planes_bytes(P) == 0) return SILENZIO_ERR_UNSUPPORTED;
+  return launch_ks_planes(ksk, planes, (int)P->ks_in_dim, (int)P->lwe_dim, (int)P->ks_base_log, (int)P->ks_level,
+                          sz_stream(stream));
+}
+
+size_t silenzio_pbs_linear_workspace_bytes(const silenzio_params *P, size_t count) {
+  if (check_params(P) != SILENZIO_OK || silenzio_ksk_planes_bytes(P) == 0) return 0;
+  return round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256) + silenzio_blind_rotate_workspace_bytes(P, count) +
+         round_up(keyswitch_tc_scratch_bytes((int)P->ks_in_dim, (int)P->ks_level, count), 256);
+}
+
+int silenzio_pbs_linear_batch(const uint64_t *in, const uint32_t *idx, const int64_t *coef, const uint64_t *cst,
+                              uint32_t terms, const uint32_t *lut_ids, const uint64_t *luts, uint32_t num_luts,
+                              const void *fbsk, const void *planes, uint64_t *out, size_t count,
+                              const silenzio_params *P, void *workspace, void *stream) {
+  SZ_RANGE("pbs_linear_batch");
+  int st = check_params(P);
+  if (st) return st;
+  if ((st = check_ks_params(P))) return st;
+  if ((st = check_br_supported(P))) return st;
+  if (P->ks_in_dim != P->glwe_dim * P->poly_size) return SILENZIO_ERR_INVALID_PARAM;
+  if (silenzio_ksk_planes_bytes(P) == 0) return SILENZIO_ERR_UNSUPPORTED;
+  if (count == 0) return SILENZIO_OK;
+  if (!in || !luts || !fbsk || !planes || !out) return SILENZIO_ERR_NULL_POINTER;
+  if (idx ? (!coef || terms == 0) : (coef || cst)) return SILENZIO_ERR_INVALID_PARAM;
+  if (!sz_aligned(in, 8) || !sz_aligned(out, 8) || !sz_aligned(luts, 8) || !sz_aligned16(planes) ||
+      !sz_aligned16(fbsk) || (lut_ids && !sz_aligned(lut_ids, 4)) || (idx && !sz_aligned(idx, 4)) ||
+      (coef && !sz_aligned(coef, 8)) || (cst && !sz_aligned(cst, 8)))
+    return SILENZIO_ERR_MISALIGNED;
+  if (count > (1ull << 31)) return SILENZIO_ERR_COUNT;
+  if (!workspace) return SILENZIO_ERR_WORKSPACE;
+  if (!sz_aligned16(workspace)) return SILENZIO_ERR_MISALIGNED;
+  u64 *small = reinterpret_cast<u64 *>(workspace);
+  unsigned char *br_ws = reinterpret_cast<unsigned char *>(workspace) + round_up(count * (size_t)(P->lwe_dim + 1) * sizeof(u64), 256);
+  unsigned char *ks_ws = br_ws + silenzio_blind_rotate_workspace_bytes(P, count);
+  {
+    SZ_RANGE("pbs.linear+keyswitch");
+    if ((st = launch_keyswitch_tc_planes(in, idx, coef, cst, (int)terms, planes, ks_ws, small, count, (int)P->ks_in_dim,
+                                         (int)P->lwe_dim, (int)P->ks_base_log, (int)P->ks_level, sz_stream(stream))))
+      return st;
   }
   return silenzio_blind_rotate_batch(small, lut_ids, luts, num_luts, fbsk, out, count, P, br_ws, stream);
 }

@@ -13,6 +13,12 @@ int silenzio_pbs_batch(const uint64_t *, const uint32_t *, const uint64_t *, uin
 int silenzio_lwe_linear_batch(const uint64_t *, const uint32_t *, const int64_t *, const uint64_t *, uint32_t,
                               uint32_t, size_t, uint64_t *, void *);
 int silenzio_build_testpoly(const uint64_t *, uint32_t, uint32_t, uint32_t, uint64_t *, void *);
+int silenzio_pbs_linear_batch(const uint64_t *, const uint32_t *, const int64_t *, const uint64_t *, uint32_t,
+                              const uint32_t *, const uint64_t *, uint32_t, const void *, const void *, uint64_t *,
+                              size_t, const silenzio_params *, void *, void *);
+size_t silenzio_pbs_linear_workspace_bytes(const silenzio_params *, size_t);
+size_t silenzio_ksk_planes_bytes(const silenzio_params *);
+int silenzio_ksk_to_planes(const uint64_t *, void *, const silenzio_params *, void *);
 size_t silenzio_pbs_workspace_bytes(const silenzio_params *, size_t);
 }
 
@@ -62,6 +68,7 @@ struct Dev {
   const silenzio_params *P;
   const void *fbsk;
   const u64 *ksk;
+  const void *planes = nullptr;  // KSK byte planes prepared once per driver call (null: silenzio_pbs_batch per lookup)
   size_t big;  // k N + 1
   // scratch
   u64 *luts;           // [kMaxLuts][N]
@@ -110,8 +117,10 @@ inline int lookup(Dev &D, const u64 *in, u64 *out, size_t count, const std::vect
       SZ_CUDA_OK(cudaStreamSynchronize(D.st));
       idp = D.ids;
     }
-    int rc = silenzio_pbs_batch(in + c0 * D.big, idp, D.luts, num_luts, D.fbsk, D.ksk, out + c0 * D.big, cnt, D.P,
-                                D.pbs_ws, D.st);
+    int rc = D.planes ? silenzio_pbs_linear_batch(in + c0 * D.big, nullptr, nullptr, nullptr, 1, idp, D.luts, num_luts,
+                                                  D.fbsk, D.planes, out + c0 * D.big, cnt, D.P, D.pbs_ws, D.st)
+                      : silenzio_pbs_batch(in + c0 * D.big, idp, D.luts, num_luts, D.fbsk, D.ksk, out + c0 * D.big,
+                                           cnt, D.P, D.pbs_ws, D.st);
     if (rc) return rc;
     if (trace_active(0))
       trace_pbs(0, in + c0 * D.big, D.big, out + c0 * D.big, D.big, D.luts, D.P->poly_size,
@@ -120,6 +129,41 @@ inline int lookup(Dev &D, const u64 *in, u64 *out, size_t count, const std::vect
   return SILENZIO_OK;
 }
 
+
+// out[i] = PBS(sum_t coef[i][t] * in[idx[i][t]] + cst[i]; luts[ids[i]]): the linear op runs inside the
+// keyswitch (silenzio_pbs_linear_batch, needs D.planes). `trace_tmp` (count ciphertexts, may be null)
+// receives the combinations only while a PBS trace is recording them.
+inline int linear_lookup(Dev &D, const u64 *in, u64 *out, size_t count, int terms, const std::vector<u32> &idx,
+                         const std::vector<i64> &coef, const std::vector<u64> &cst, const std::vector<u32> &ids,
+                         u32 num_luts, u64 *trace_tmp) {
+  if (count == 0) return SILENZIO_OK;
+  if (!D.planes || (trace_active(0) && trace_tmp)) {  // unfused: the trace records the PBS inputs
+    if (!trace_tmp) return SILENZIO_ERR_WORKSPACE;
+    int rc = linear(D, in, trace_tmp, count, terms, idx, coef, cst);
+    if (rc) return rc;
+    return lookup(D, trace_tmp, out, count, ids, num_luts);
+  }
+  if (count * terms > D.idx_cap || count > D.idx_cap) return SILENZIO_ERR_WORKSPACE;
+  SZ_CUDA_OK(cudaMemcpyAsync(D.idx, idx.data(), count * terms * 4, cudaMemcpyHostToDevice, D.st));
+  SZ_CUDA_OK(cudaMemcpyAsync(D.coef, coef.data(), count * terms * 8, cudaMemcpyHostToDevice, D.st));
+  SZ_CUDA_OK(cudaMemcpyAsync(D.cst, cst.data(), count * 8, cudaMemcpyHostToDevice, D.st));
+  const size_t chunk = D.pbs_cap;
+  for (size_t c0 = 0; c0 < count; c0 += chunk) {
+    const size_t cnt = count - c0 < chunk ? count - c0 : chunk;
+    const u32 *idp = nullptr;
+    if (!ids.empty()) {
+      if (cnt > D.ids_cap) return SILENZIO_ERR_WORKSPACE;
+      SZ_CUDA_OK(cudaMemcpyAsync(D.ids, ids.data() + c0, cnt * 4, cudaMemcpyHostToDevice, D.st));
+      idp = D.ids;
+    }
+    int rc = silenzio_pbs_linear_batch(in, D.idx + c0 * terms, D.coef + c0 * terms, D.cst + c0, (u32)terms, idp, D.luts,
+                                       num_luts, D.fbsk, D.planes, out + c0 * D.big, cnt, D.P, D.pbs_ws, D.st);
+    if (rc) return rc;
+  }
+  // the staging buffers are reused by the next call and the host vectors die with the caller
+  SZ_CUDA_OK(cudaStreamSynchronize(D.st));
+  return SILENZIO_OK;
+}
 
 // out[e] = ca A[e] + cb B[e] + cc C[e] + cst (elementwise over `count` ciphertexts; null arrays skipped)
 inline int axpy3(Dev &D, u64 *out, const u64 *A, i64 ca, const u64 *B, i64 cb, const u64 *C, i64 cc, u64 cst,

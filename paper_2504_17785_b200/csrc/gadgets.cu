@@ -43,11 +43,11 @@ int sum_tree(Dev &D, int m, u64 *buf, u64 *tmp, u64 *tmp2, size_t groups, size_t
             idx[(q * next + o) * g + t] = (u32)(q * cur + (src < cur ? src : 0));
             coef[(q * next + o) * g + t] = src < cur ? 1 : 0;
           }
-      int rc = linear(D, buf, tmp, groups * next, (int)g, idx, coef, cst);
-      if (rc) return rc;
       std::vector<std::vector<u64>> tabs = {table_window(0, [m](int s) { return enc(pmod(s, m), kDelta); })};
-      if ((rc = upload_luts(D, tabs))) return rc;
-      if ((rc = lookup(D, tmp, buf, groups * next, {}, 1))) return rc;
+      int rc = upload_luts(D, tabs);
+      if (rc) return rc;
+      // in place: the keyswitch stage consumes every input before the blind rotation writes buf
+      if ((rc = linear_lookup(D, buf, buf, groups * next, (int)g, idx, coef, cst, {}, 1, tmp))) return rc;
       cur = next;
     } else {
       // pair tree with the sign trick T3: t = x + y - m; s = sign PBS(t) * m Delta/2;
@@ -71,15 +71,12 @@ int sum_tree(Dev &D, int m, u64 *buf, u64 *tmp, u64 *tmp2, size_t groups, size_t
       if (rc) return rc;
       std::vector<std::vector<u64>> tabs = {std::vector<u64>(16, half_m)};  // T2 sign
       if ((rc = upload_luts(D, tabs))) return rc;
-      if ((rc = lookup(D, tmp, tmp2, groups * next, {}, 1))) return rc;  // s
+      // s lands right after t in tmp, so the second linear op addresses both through one base
+      if ((rc = lookup(D, tmp, tmp + groups * next * D.big, groups * next, {}, 1))) return rc;  // s
       // z = t + m Delta/2 - s
       std::vector<u32> idx2(groups * next * 2);
       std::vector<i64> coef2(groups * next * 2);
       std::vector<u64> cst2(groups * next, half_m);
-      // linear() reads one input array: place t and s side by side by
-      // addressing tmp (t) and tmp2 (s) through one base: copy s after t
-      SZ_CUDA_OK(cudaMemcpyAsync(tmp + groups * next * D.big, tmp2, groups * next * D.big * 8,
-                                 cudaMemcpyDeviceToDevice, D.st));
       for (size_t e = 0; e < groups * next; e++) {
         idx2[e * 2] = (u32)e;
         idx2[e * 2 + 1] = (u32)(groups * next + e);
@@ -121,7 +118,7 @@ size_t silenzio_rns_matmul_workspace_bytes(const silenzio_params *P, uint32_t a,
   const size_t idx_cap = 2 * prod;
   const size_t pbs_cap = 65536;
   return bufs * ct + idx_cap * (4 + 8) + idx_cap * 8 + pbs_cap * 4 + kMaxLuts * (P->poly_size + 16) * 8 +
-         silenzio_pbs_workspace_bytes(P, pbs_cap) + 4096;
+         silenzio_pbs_workspace_bytes(P, pbs_cap) + silenzio_ksk_planes_bytes(P) + 4096;
 }
 
 int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32_t b, uint32_t c,
@@ -169,6 +166,14 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
   D.tables = reinterpret_cast<u64 *>(carve(kMaxLuts * 16 * 8));
   D.luts = reinterpret_cast<u64 *>(carve((size_t)kMaxLuts * P->poly_size * 8));
   D.pbs_ws = carve(silenzio_pbs_workspace_bytes(P, D.pbs_cap));
+  // KSK byte planes once per call (not once per PBS launch); every "linear op, then lookup"
+  // below is then one silenzio_pbs_linear_batch (a0 fused into a1)
+  if (const size_t pb = silenzio_ksk_planes_bytes(P)) {
+    void *planes = carve(pb);
+    int prc = silenzio_ksk_to_planes(ksk, planes, P, D.st);
+    if (prc) return prc;
+    D.planes = planes;
+  }
 
   const size_t nX = (size_t)a * b, nW = (size_t)b * c;
   int rc;
@@ -233,13 +238,12 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
               ids[o] = (u32)h;
             }
           }
-        if ((rc = linear(D, T3, T0, 2 * np, 2, idx, coef, cst))) return rc;
         const int i4 = inv4(m);
         std::vector<std::vector<u64>> tabs = {
             table_window(0, [m, i4](int s) { return enc(pmod((long)i4 * s * s, m), kDelta); }),
             table_window(-8, [m, i4](int d) { return enc(pmod(-(long)i4 * d * d, m), kDelta); })};
         if ((rc = upload_luts(D, tabs))) return rc;
-        if ((rc = lookup(D, T0, T1, 2 * np, ids, 2))) return rc;
+        if ((rc = linear_lookup(D, T3, T1, 2 * np, 2, idx, coef, cst, ids, 2, T0))) return rc;
         terms_per_product = 2;
       } else if (m == 16) {
         // q00 = 4 a0 + b0, q01 = 4 a0 + b1, q10 = 4 a1 + b0; digit products at 2^60
@@ -261,12 +265,11 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
               ids[o] = h == 0 ? 0u : 1u;
             }
           }
-        if ((rc = linear(D, T3, T0, 3 * np, 2, idx, coef, cst))) return rc;
         std::vector<std::vector<u64>> tabs = {
             table_window(0, [](int q) { return enc(((q >> 2) * (q & 3)) & 15, kDelta16); }),
             table_window(0, [](int q) { return enc((4 * (q >> 2) * (q & 3)) & 15, kDelta16); })};
         if ((rc = upload_luts(D, tabs))) return rc;
-        if ((rc = lookup(D, T0, T1, 3 * np, ids, 2))) return rc;
+        if ((rc = linear_lookup(D, T3, T1, 3 * np, 2, idx, coef, cst, ids, 2, T0))) return rc;
         terms_per_product = 3;
       } else {
         // m in {9, 11, 13}: t1 = x + w - m, t2 = x - w; sigma = sign PBS; u, v = T3(t);
@@ -302,7 +305,6 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
           coef2[2 * o] = 1;
           coef2[2 * o + 1] = -1;
         }
-        if ((rc = linear(D, T0, T2, 2 * np, 2, idx2, coef2, cst2))) return rc;
         const int i4 = inv4(m);
         std::vector<std::vector<u64>> tabs2 = {
             table_window(0, [m, i4](int s) { return enc(pmod((long)i4 * s * s, m), kDelta); }),
@@ -310,7 +312,7 @@ int silenzio_rns_matmul(const uint64_t *X, const uint64_t *W, uint32_t a, uint32
         if ((rc = upload_luts(D, tabs2))) return rc;
         std::vector<u32> ids(2 * np);
         for (size_t o = 0; o < 2 * np; o++) ids[o] = (u32)(o & 1);
-        if ((rc = lookup(D, T2, T1, 2 * np, ids, 2))) return rc;
+        if ((rc = linear_lookup(D, T0, T1, 2 * np, 2, idx2, coef2, cst2, ids, 2, T2))) return rc;
         terms_per_product = 2;
       }
       // ---------------- g3: modular summation of the b * terms_per_product terms of each output j

@@ -93,9 +93,28 @@ __global__ void ks_planes_kernel(const u64 *ksk, unsigned char *planes, int K, i
 // K index k = jj l + t - 1 for coefficient j = 32 stage + jj (signed digit of
 // level t, C3 decomposition). One thread per (ciphertext, stage, half of the
 // stage's 32 coefficients): 16 coefficients -> 16 l digit bytes.
+// Optional linear prologue (SURVEY.md §8(a) a0 fused into a1): with lin.idx set,
+// row r of the keyswitch input is sum_t coef[r][t] * in[idx[r][t]] + (0,..,0,cst[r])
+// mod 2^64, formed on the fly (the combination never goes through HBM); its
+// body is written to bodies[r] for the GEMM epilogue.
+struct Lin {
+  const u32 *idx;   // [count][terms] rows of `in`, or null (row r is in[r])
+  const i64 *coef;  // [count][terms]
+  const u64 *cst;   // [count] or null
+  int terms;
+};
+__device__ __forceinline__ u64 lin_value(const u64 *in, const Lin &lin, long row, int in_dim, int j) {
+  if (!lin.idx) return __ldg(in + (size_t)row * (in_dim + 1) + j);
+  u64 v = 0;
+  for (int t = 0; t < lin.terms; t++) {
+    const size_t o = (size_t)row * lin.terms + t;
+    v += (u64)__ldg(lin.coef + o) * __ldg(in + (size_t)__ldg(lin.idx + o) * (in_dim + 1) + j);
+  }
+  return v;
+}
 template <int L>
-__global__ void ks_digits_kernel(const u64 *in, unsigned char *digits, long count, int rows_padded, int in_dim,
-                                 int base_log) {
+__global__ void ks_digits_kernel(const u64 *in, Lin lin, u64 *bodies, unsigned char *digits, long count,
+                                 int rows_padded, int in_dim, int base_log) {
   constexpr int KST = stage_k(L);
   const int nst = in_dim / kJ;
   const long total = (long)rows_padded * nst * 2;
@@ -105,13 +124,13 @@ __global__ void ks_digits_kernel(const u64 *in, unsigned char *digits, long coun
     const long row = rest % rows_padded;
     const int st = (int)(rest / rows_padded);
     const bool live = row < count;
-    const u64 *arow = in + (size_t)(live ? row : 0) * (in_dim + 1) + kJ * st + 16 * h;
+    const int j0 = kJ * st + 16 * h;
     uint32_t w[4 * L];
 #pragma unroll
     for (int q = 0; q < 4 * L; q++) w[q] = 0;
 #pragma unroll
     for (int jj = 0; jj < 16; jj++) {
-      u64 rr = sz_decomp_round(live ? __ldg(arow + jj) : 0ull, base_log, L);
+      u64 rr = sz_decomp_round(live ? lin_value(in, lin, row, in_dim, j0 + jj) : 0ull, base_log, L);
 #pragma unroll
       for (int t = L; t >= 1; t--) {
         const int d = (int)sz_decomp_next(rr, base_log);
@@ -119,6 +138,8 @@ __global__ void ks_digits_kernel(const u64 *in, unsigned char *digits, long coun
         w[k >> 2] |= (uint32_t)(d & 0xff) << (8 * (k & 3));
       }
     }
+    if (bodies && live && st == 0 && h == 0)
+      bodies[row] = lin_value(in, lin, row, in_dim, in_dim) + (lin.cst ? __ldg(lin.cst + row) : 0ull);
     unsigned char *tile = digits + ((size_t)(row / kRows) * nst + st) * a_tile(L);
     const int r = (int)(row % kRows);
 #pragma unroll
@@ -187,6 +208,7 @@ struct Args {
   const u64 *in;                // [count][in_dim+1]
   const unsigned char *planes;  // [ncb][nst][b_tile]
   const unsigned char *digits;  // [row tiles][nst][a_tile]
+  const u64 *bodies;            // [count] input bodies (linear prologue), or null: in[row][in_dim]
   u64 *out;                     // [count][n+1]
   long count;
   int in_dim, n1, base_log, level;
@@ -274,12 +296,15 @@ __global__ void __launch_bounds__(kThreads, 1) keyswitch_tc_kernel(Args A) {
     for (int c = 0; c < 16; c++) acc[c] += (u64)(i64)(int32_t)v[c] << (8 * b);
   }
   if (ecrow < A.count) {
-    const u64 *irow = A.in + (size_t)ecrow * (A.in_dim + 1);
     u64 *orow = A.out + (size_t)ecrow * A.n1;
 #pragma unroll
     for (int c = 0; c < 16; c++) {
       const int col = cb * kCols + 16 * half + c;
-      if (col < A.n1) orow[col] = ((col == A.n1 - 1) ? irow[A.in_dim] : 0ull) - acc[c];
+      if (col < A.n1) {
+        u64 body = 0;
+        if (col == A.n1 - 1) body = A.bodies ? A.bodies[ecrow] : A.in[(size_t)ecrow * (A.in_dim + 1) + A.in_dim];
+        orow[col] = body - acc[c];
+      }
     }
   }
   tmem_fence_before();
@@ -309,21 +334,42 @@ size_t keyswitch_tc_workspace_bytes(int in_dim, int n, int level, int base_log, 
   return ks_planes_bytes(in_dim, n, level) + rows * (size_t)in_dim * level;
 }
 
-int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, int in_dim, int n, int base_log,
-                        int level, void *workspace, cudaStream_t stream) {
+// KSK -> byte planes in the tensor-core operand layout (once per key, or per call by launch_keyswitch_tc)
+size_t keyswitch_tc_planes_bytes(int in_dim, int n, int level, int base_log) {
+  return ks_tc_applicable(in_dim, level, base_log) ? ks_planes_bytes(in_dim, n, level) : 0;
+}
+int launch_ks_planes(const u64 *ksk, void *planes_, int in_dim, int n, int base_log, int level, cudaStream_t stream) {
   if (!ks_tc_applicable(in_dim, level, base_log)) return SILENZIO_ERR_UNSUPPORTED;
-  if (((uintptr_t)workspace & 15) != 0) return SILENZIO_ERR_MISALIGNED;
   const int n1 = n + 1, K = in_dim * level;
   const int ncb = (n1 + kst::kCols - 1) / kst::kCols;
-  unsigned char *planes = reinterpret_cast<unsigned char *>(workspace);
-  unsigned char *digits = planes + ks_planes_bytes(in_dim, n, level);
-  {
-    const long total = (long)ncb * (K / kst::stage_k(level)) * kst::kCols * (kst::stage_k(level) / 16);
-    const int threads = 256;
-    const long blocks = (total + threads - 1) / threads;
-    kst::ks_planes_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, stream>>>(ksk, planes, K, n1, level, ncb);
-    SZ_LAUNCH_OK();
-  }
+  const long total = (long)ncb * (K / kst::stage_k(level)) * kst::kCols * (kst::stage_k(level) / 16);
+  const int threads = 256;
+  const long blocks = (total + threads - 1) / threads;
+  kst::ks_planes_kernel<<<(unsigned)(blocks < 65535 * 16 ? blocks : 65535 * 16), threads, 0, stream>>>(
+      ksk, reinterpret_cast<unsigned char *>(planes_), K, n1, level, ncb);
+  SZ_LAUNCH_OK();
+  return SILENZIO_OK;
+}
+
+// scratch of the product itself: digit matrix, then (linear prologue only) the input bodies
+size_t keyswitch_tc_scratch_bytes(int in_dim, int level, size_t count) {
+  const size_t rows = (count + kst::kRows - 1) / kst::kRows * kst::kRows;
+  return rows * (size_t)in_dim * level + rows * sizeof(u64);
+}
+
+// out = keyswitch of (the linear combinations of) `in` with prepared byte planes.
+// idx == null: row r = in[r]. scratch: keyswitch_tc_scratch_bytes, 16-byte aligned.
+int launch_keyswitch_tc_planes(const u64 *in, const u32 *idx, const i64 *coef, const u64 *cst, int terms,
+                               const void *planes_, void *scratch, u64 *out, size_t count, int in_dim, int n,
+                               int base_log, int level, cudaStream_t stream) {
+  if (!ks_tc_applicable(in_dim, level, base_log)) return SILENZIO_ERR_UNSUPPORTED;
+  if (((uintptr_t)planes_ & 15) != 0 || ((uintptr_t)scratch & 15) != 0) return SILENZIO_ERR_MISALIGNED;
+  const int n1 = n + 1;
+  const int ncb = (n1 + kst::kCols - 1) / kst::kCols;
+  const unsigned char *planes = reinterpret_cast<const unsigned char *>(planes_);
+  unsigned char *digits = reinterpret_cast<unsigned char *>(scratch);
+  const size_t rows_all = (count + kst::kRows - 1) / kst::kRows * kst::kRows;
+  u64 *bodies = idx ? reinterpret_cast<u64 *>(digits + rows_all * (size_t)in_dim * level) : nullptr;
   void (*kern)(kst::Args) = nullptr;
   switch (level) {
     case 1: kern = kst::keyswitch_tc_kernel<1>; break;
@@ -336,7 +382,7 @@ int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, i
   }
   const size_t smem = kst::smem_bytes(level);
   SZ_CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  void (*dkern)(const u64 *, unsigned char *, long, int, int, int) = nullptr;
+  void (*dkern)(const u64 *, kst::Lin, u64 *, unsigned char *, long, int, int, int) = nullptr;
   switch (level) {
     case 1: dkern = kst::ks_digits_kernel<1>; break;
     case 2: dkern = kst::ks_digits_kernel<2>; break;
@@ -350,19 +396,36 @@ int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, i
   for (size_t c0 = 0; c0 < count; c0 += max_rows) {
     const size_t cnt = count - c0 < max_rows ? count - c0 : max_rows;
     const int rows_padded = (int)((cnt + kst::kRows - 1) / kst::kRows * kst::kRows);
+    // with the prologue, rows address `in` through idx (not offset by c0); without it, row r is in[c0 + r]
+    const u64 *in_c = idx ? in : in + c0 * (size_t)(in_dim + 1);
+    kst::Lin lin{idx ? idx + c0 * (size_t)terms : nullptr, idx ? coef + c0 * (size_t)terms : nullptr,
+                 (idx && cst) ? cst + c0 : nullptr, terms};
     {
       const long total = (long)rows_padded * (in_dim / kst::kJ) * 2;
       const long blocks = (total + 255) / 256;
       dkern<<<(unsigned)(blocks < 65535L * 64 ? blocks : 65535L * 64), 256, 0, stream>>>(
-          in + c0 * (size_t)(in_dim + 1), digits, (long)cnt, rows_padded, in_dim, base_log);
+          in_c, lin, bodies ? bodies + c0 : nullptr, digits, (long)cnt, rows_padded, in_dim, base_log);
       SZ_LAUNCH_OK();
     }
-    kst::Args A{in + c0 * (size_t)(in_dim + 1), planes, digits, out + c0 * (size_t)n1, (long)cnt, in_dim, n1, base_log, level};
+    kst::Args A{in_c, planes, digits, bodies ? bodies + c0 : nullptr, out + c0 * (size_t)n1, (long)cnt, in_dim, n1,
+                base_log, level};
     dim3 grid((unsigned)ncb, (unsigned)((cnt + kst::kRows - 1) / kst::kRows));
     kern<<<grid, kst::kThreads, smem, stream>>>(A);
     SZ_LAUNCH_OK();
   }
   return SILENZIO_OK;
+}
+
+// planes re-derived from the KSK into the workspace on every call (silenzio_keyswitch_batch, silenzio_pbs_batch)
+int launch_keyswitch_tc(const u64 *in, const u64 *ksk, u64 *out, size_t count, int in_dim, int n, int base_log,
+                        int level, void *workspace, cudaStream_t stream) {
+  if (!ks_tc_applicable(in_dim, level, base_log)) return SILENZIO_ERR_UNSUPPORTED;
+  if (((uintptr_t)workspace & 15) != 0) return SILENZIO_ERR_MISALIGNED;
+  unsigned char *planes = reinterpret_cast<unsigned char *>(workspace);
+  int rc = launch_ks_planes(ksk, planes, in_dim, n, base_log, level, stream);
+  if (rc) return rc;
+  return launch_keyswitch_tc_planes(in, nullptr, nullptr, nullptr, 1, planes, planes + ks_planes_bytes(in_dim, n, level),
+                                    out, count, in_dim, n, base_log, level, stream);
 }
 
 }  // namespace sz

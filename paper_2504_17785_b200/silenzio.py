@@ -54,6 +54,10 @@ def load():
         "silenzio_pbs_batch_host": ([V, V, V, U32, V, V, V, S, S, P, V, V], I),
         "silenzio_lwe_linear_batch": ([V, V, V, V, U32, U32, S, V, V], I),
         "silenzio_build_testpoly": ([V, U32, U32, U32, V, V], I),
+        "silenzio_ksk_planes_bytes": ([P], S),
+        "silenzio_ksk_to_planes": ([V, V, P, V], I),
+        "silenzio_pbs_linear_workspace_bytes": ([P, S], S),
+        "silenzio_pbs_linear_batch": ([V, V, V, V, U32, V, V, U32, V, V, V, S, P, V, V], I),
         "silenzio_lwe_encrypt_batch": ([V, V, V, V, U32, S, V, V], I),
         "silenzio_lwe_phase_batch": ([V, V, U32, S, V, V], I),
         "silenzio_bsk_generate": ([V, V, V, V, V, P, V, V], I),
@@ -96,7 +100,8 @@ def exported_symbols():
         "silenzio_pbs_workspace_bytes", "silenzio_pbs_host_workspace_bytes", "silenzio_pbs_launch_count",
         "silenzio_bsk_to_fourier", "silenzio_keyswitch_batch", "silenzio_keyswitch_workspace_bytes", "silenzio_pbs_batch",
         "silenzio_blind_rotate_batch", "silenzio_blind_rotate_workspace_bytes", "silenzio_pbs_batch_host", "silenzio_lwe_linear_batch",
-        "silenzio_build_testpoly", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
+        "silenzio_build_testpoly", "silenzio_ksk_planes_bytes", "silenzio_ksk_to_planes",
+        "silenzio_pbs_linear_workspace_bytes", "silenzio_pbs_linear_batch", "silenzio_lwe_encrypt_batch", "silenzio_lwe_phase_batch",
         "silenzio_bsk_generate", "silenzio_bsk_generate_workspace_bytes", "silenzio_ksk_generate", "silenzio_rns_matmul_workspace_bytes",
         "silenzio_rns_matmul", "silenzio_gadget_workspace_bytes", "silenzio_rns2mrns",
         "silenzio_rns_sign_abs", "silenzio_mrns_bitlen_max", "silenzio_int_ce_grad",
@@ -274,6 +279,67 @@ def lwe_linear_batch(lwe_in, idx, coef, cst, out=None, stream=None):
         out = torch.empty((count, dim + 1), dtype=torch.int64, device=lwe_in.device)
     _check(load().silenzio_lwe_linear_batch(_ptr(lwe_in), _ptr(idx), _ptr(coef), _ptr(cst), terms, dim, count,
                                             _ptr(out), _stream(stream)))
+    return out
+
+
+def ksk_planes_bytes(P) -> int:
+    return load().silenzio_ksk_planes_bytes(ctypes.byref(make_params(P)))
+
+
+def ksk_to_planes(ksk, P, planes=None, stream=None):
+    """Once-per-key KSK byte planes for silenzio_pbs_linear_batch."""
+    nb = ksk_planes_bytes(P)
+    if nb == 0:
+        raise SilenzioError("no tensor-core keyswitch for these parameters (silenzio_ksk_planes_bytes = 0)")
+    if planes is None:
+        planes = torch.empty(nb, dtype=torch.uint8, device=ksk.device)
+    elif planes.numel() * planes.element_size() < nb:
+        raise SilenzioError("planes buffer too small (silenzio_ksk_planes_bytes)")
+    _check(load().silenzio_ksk_to_planes(_ptr(ksk), _ptr(planes), ctypes.byref(make_params(P)), _stream(stream)))
+    return planes
+
+
+def pbs_linear_workspace_bytes(P, count: int) -> int:
+    return load().silenzio_pbs_linear_workspace_bytes(ctypes.byref(make_params(P)), count)
+
+
+def pbs_linear_batch(lwe_in, idx, coef, cst, lut_ids, luts, fourier_bsk, ksk_planes, P, out=None, workspace=None,
+                     stream=None):
+    """PBS of sum_t coef[i][t] * lwe_in[idx[i][t]] + cst[i] (idx None: of lwe_in[i]) with prepared KSK planes."""
+    big = P.k * P.N + 1
+    if lwe_in.dtype != torch.int64 or lwe_in.dim() != 2 or lwe_in.shape[1] != big:
+        raise SilenzioError(f"lwe_in must be int64 [*][{big}]")
+    if idx is not None:
+        if idx.dtype != torch.int32 or idx.dim() != 2:
+            raise SilenzioError("idx must be int32 [count][terms]")
+        count, terms = idx.shape
+        if coef is None or coef.dtype != torch.int64 or tuple(coef.shape) != (count, terms):
+            raise SilenzioError("coef must be int64 [count][terms]")
+        if cst is not None and (cst.dtype != torch.int64 or cst.numel() != count):
+            raise SilenzioError("cst must be int64 [count]")
+        if count and (int(idx.min()) < 0 or int(idx.max()) >= lwe_in.shape[0]):
+            raise SilenzioError("idx out of range")
+    else:
+        if coef is not None or cst is not None:
+            raise SilenzioError("coef / cst need idx")
+        count, terms = lwe_in.shape[0], 1
+    if lut_ids is not None and (lut_ids.dtype != torch.int32 or lut_ids.numel() != count):
+        raise SilenzioError("lut_ids must be int32 [count]")
+    if luts.dtype != torch.int64 or luts.shape[-1] != P.N:
+        raise SilenzioError(f"luts must be int64 [num_luts][{P.N}]")
+    if out is None:
+        out = torch.empty((count, big), dtype=torch.int64, device=lwe_in.device)
+    elif out.dtype != torch.int64 or tuple(out.shape) != (count, big):
+        raise SilenzioError(f"out must be int64 [{count}][{big}]")
+    need = pbs_linear_workspace_bytes(P, count)
+    if workspace is None:
+        workspace = torch.empty(need, dtype=torch.uint8, device=lwe_in.device)
+    elif workspace.numel() * workspace.element_size() < need:
+        raise SilenzioError("workspace too small (silenzio_pbs_linear_workspace_bytes)")
+    num_luts = luts.shape[0] if luts.dim() == 2 else 1
+    _check(load().silenzio_pbs_linear_batch(_ptr(lwe_in), _ptr(idx), _ptr(coef), _ptr(cst), terms, _ptr(lut_ids),
+                                            _ptr(luts), num_luts, _ptr(fourier_bsk), _ptr(ksk_planes), _ptr(out),
+                                            count, ctypes.byref(make_params(P)), _ptr(workspace), _stream(stream)))
     return out
 
 

@@ -76,3 +76,56 @@ def test_pbs_fewer_fft_limbs_still_decrypt(limbs, bits, dev):
     out = silenzio.pbs_batch(ct, torch.from_numpy(ids.astype(np.int32)).to(dev), luts, keys["fbsk"], keys["ksk"], P)
     dec = wl.decode(wl.to_host_u64(silenzio.lwe_phase_batch(out, keys["big_key"])), P.p)
     assert np.array_equal(dec, tabs[ids, m])
+
+
+def test_pbs_linear_batch_fused_prologue(dev):
+    """silenzio_pbs_linear_batch (SURVEY §8(a) a0 fused into a1, prepared KSK byte planes):
+    its keyswitch stage equals the oracle's lwe_linear + keyswitch bit for bit (integer
+    stages), the whole call equals silenzio_lwe_linear_batch followed by silenzio_pbs_batch
+    bit for bit, sampled outputs agree with the oracle PBS of the oracle's combination
+    within 2^-32, and idx = NULL is the plain PBS. Ragged count (not a multiple of the
+    128-row tensor-core tile), negative coefficients, constants, repeated inputs."""
+    from paper_2504_17785_b200 import silenzio, workload as wl
+    P = get_params("A_SMALLN")
+    rnd = key_randomness(P, 171)
+    keys = wl.device_keys(P, rnd, dev)
+    ok = oracle.keygen(P, rnd)
+    n_in, count, terms = 90, 301, 3
+    rng = np.random.default_rng(172)
+    # inputs hold messages in [0, 4) so that x = a + b - c + cst stays inside the 4-bit window
+    m = rng.integers(0, 4, size=n_in)
+    r = lwe_randomness(P, n_in, 173)
+    ct = oracle.lwe_encrypt(oracle.encode(m, P.p), ok["big_key"], r["mask"], r["noise"])
+    idx = rng.integers(0, n_in, size=(count, terms)).astype(np.uint32)
+    coef = np.tile(np.array([1, 1, -1], dtype=np.int64), (count, 1))
+    coef[::7, 1] = 2
+    cst_m = rng.integers(3, 6, size=count)
+    cst = oracle.encode(cst_m, P.p)
+    tabs = lut_tables(8, P.p, 174)
+    luts = wl.luts_from_tables(tabs, P.p, P.N, dev)
+    ids = lut_ids(count, 8, 175)
+    x_m = (m[idx].astype(np.int64) * coef).sum(axis=1) + cst_m
+    assert x_m.min() >= 0 and x_m.max() < 16
+    planes = silenzio.ksk_to_planes(keys["ksk"], P)
+    d = lambda a: wl.to_dev(a, dev)
+    idx_d, coef_d, cst_d = d(idx.view(np.int32)), d(coef), d(cst)
+    ids_d = torch.from_numpy(ids.astype(np.int32)).to(dev)
+    fused = silenzio.pbs_linear_batch(d(ct), idx_d, coef_d, cst_d, ids_d, luts, keys["fbsk"], planes, P)
+    lin = silenzio.lwe_linear_batch(d(ct), idx_d, coef_d, cst_d)
+    two = silenzio.pbs_batch(lin, ids_d, luts, keys["fbsk"], keys["ksk"], P)
+    assert torch.equal(fused, two)
+    # the oracle's combination, bit-exact with the GPU linear kernel, then sampled oracle PBS
+    lin_o = oracle.lwe_linear(ct, idx, coef, cst)
+    assert np.array_equal(wl.to_host_u64(lin), lin_o)
+    out_g = wl.to_host_u64(fused)
+    assert np.array_equal(oracle.lwe_decrypt(out_g, ok["big_key"], P.p), tabs[ids, x_m])
+    sample = np.array([0, 1, 127, 128, 255, 256, 300])
+    vs = np.stack([oracle.test_polynomial(oracle.encode(tabs[l], P.p), P.p, P.N) for l in range(8)])
+    out_o = oracle.pbs(lin_o[sample], ids[sample], vs, ok["bsk"], ok["ksk"], P)
+    dphi = oracle.torus_diff(oracle.lwe_phase(out_g[sample], ok["big_key"]), oracle.lwe_phase(out_o, ok["big_key"]))
+    assert np.abs(dphi).max() <= 2 ** 32
+    # idx = NULL: plain PBS of the rows, in place
+    plain = silenzio.pbs_batch(lin, ids_d, luts, keys["fbsk"], keys["ksk"], P)
+    buf = lin.clone()
+    silenzio.pbs_linear_batch(buf, None, None, None, ids_d, luts, keys["fbsk"], planes, P, out=buf)
+    assert torch.equal(buf, plain)
