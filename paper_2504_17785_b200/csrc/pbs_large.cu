@@ -248,12 +248,23 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
 #pragma unroll 1
       for (int r = 0; r < 2; r++) {
         const u64 *accr = acc + r * kNL;
+        // L = 2: the level-1 pass decomposes every coefficient once and keeps the
+        // level-2 digits (|d| <= 2^{base_log-1} < 2^15) as packed int16 pairs for the
+        // level-2 pass (no second read of the rotated ACC, no second decomposition)
+        constexpr bool kPack = (L == 2);
+        uint32_t pk[kPack ? 16 : 1];
 #pragma unroll 1
         for (int lvl = 1; lvl <= L; lvl++) {
           double2 x[16];
+          if (kPack && lvl == 2 && blog <= 15) {
+#pragma unroll
+            for (int m = 0; m < 16; m++)
+              x[m] = make_double2((double)(short)(pk[kPack ? m : 0] & 0xffffu), (double)(short)(pk[kPack ? m : 0] >> 16));
+          } else {
 #pragma unroll
           for (int m = 0; m < 16; m++) {
             double dv[2];
+            int d2[2] = {0, 0};
 #pragma unroll
             for (int h = 0; h < 2; h++) {
               const int j = t + 256 * m + 4096 * h;
@@ -266,10 +277,13 @@ __global__ void __launch_bounds__(256, 1) blind_rotate_large_kernel(BRLArgs A) {
               for (int tt = L; tt >= 1; tt--) {
                 const i64 dd = sz_decomp_next(rr, blog);
                 if (tt == lvl) d = dd;
+                if (kPack && tt == 2) d2[h] = (int)dd;
               }
               dv[h] = (double)d;
             }
             x[m] = make_double2(dv[0], dv[1]);
+            if (kPack) pk[m] = ((uint32_t)d2[0] & 0xffffu) | ((uint32_t)d2[1] << 16);
+          }
           }
           fwd_fft_L(x, buf, t);
           const int row = r * L + (lvl - 1);
