@@ -105,6 +105,101 @@ __device__ __forceinline__ void dft(double2 (&x)[R]) {
   dft_stage<R, INV, R / 2>(x);
 }
 
+// ---- FMA-form radix-2 decimation-in-time butterflies (6 FP64 instructions when
+// the twiddle is nontrivial, against 8 for "add, subtract, multiply"): with
+// W^e = i^q e^{i theta}, |theta| <= pi/4 after pulling out i^q,
+//   e^{i theta} b = cos (b.x - tan b.y, b.y + tan b.x) = sin (cot b.x - b.y, cot b.y + b.x)
+// and the cos / sin factor folds into the four output FMAs. W = e^{+2 pi i / 32}.
+struct FmaTw32 {
+  // cos(2 pi r / 32), tan(2 pi r / 32), r = 0..4 (correctly rounded doubles)
+  static constexpr double c[5] = {1.0, 0.9807852804032304, 0.9238795325112867, 0.8314696123025452,
+                                  0.7071067811865476};
+  static constexpr double t[5] = {0.0, 0.198912367379658, 0.41421356237309503, 0.6681786379192989, 1.0};
+};
+template <int E, bool INV>
+__device__ __forceinline__ void bfly32(double2 &a, double2 &b) {
+  constexpr int e = INV ? ((32 - (E & 31)) & 31) : (E & 31);
+  constexpr int q = e >> 3, r = e & 7;
+  if constexpr (r == 0) {
+    double2 t;
+    if constexpr (q == 0) t = b;
+    else if constexpr (q == 1) t = make_double2(-b.y, b.x);
+    else if constexpr (q == 2) t = make_double2(-b.x, -b.y);
+    else t = make_double2(b.y, -b.x);
+    const double2 na = cadd(a, t), nb = csub(a, t);
+    a = na;
+    b = nb;
+  } else {
+    double u, v;
+    if constexpr (r <= 4) {
+      constexpr double tn = FmaTw32::t[r];
+      u = fma(-tn, b.y, b.x);
+      v = fma(tn, b.x, b.y);
+    } else {
+      constexpr double ct = FmaTw32::t[8 - r];
+      u = fma(ct, b.x, -b.y);
+      v = fma(ct, b.y, b.x);
+    }
+    constexpr double f = (r <= 4) ? FmaTw32::c[r] : FmaTw32::c[8 - r];
+    double U, V;  // (u + i v) * i^q
+    if constexpr (q == 0) { U = u; V = v; }
+    else if constexpr (q == 1) { U = -v; V = u; }
+    else if constexpr (q == 2) { U = -u; V = -v; }
+    else { U = v; V = -u; }
+    const double2 na = make_double2(fma(f, U, a.x), fma(f, V, a.y));
+    const double2 nb = make_double2(fma(-f, U, a.x), fma(-f, V, a.y));
+    a = na;
+    b = nb;
+  }
+}
+template <bool INV>
+__device__ __forceinline__ void bfly32_v(double2 &a, double2 &b, int e) {
+  switch (e & 31) {
+#define SZ_B32(k) \
+  case k: bfly32<k, INV>(a, b); break;
+    SZ_B32(0) SZ_B32(2) SZ_B32(4) SZ_B32(6) SZ_B32(8) SZ_B32(10) SZ_B32(12) SZ_B32(14)
+#undef SZ_B32
+    default: break;
+  }
+}
+template <bool INV, int H>
+__device__ __forceinline__ void dit16_stage(double2 (&y)[16]) {
+  if constexpr (H <= 8) {
+#pragma unroll
+    for (int b = 0; b < 16; b += 2 * H)
+#pragma unroll
+      for (int j = 0; j < H; j++) bfly32_v<INV>(y[b + j], y[b + j + H], j * (16 / H));
+    dit16_stage<INV, 2 * H>(y);
+  }
+}
+
+__host__ __device__ constexpr int bitrev4_(int r) {
+  return ((r & 1) << 3) | ((r & 2) << 1) | ((r & 4) >> 1) | ((r & 8) >> 3);
+}
+#ifndef SZ_DFT16_FMA
+#define SZ_DFT16_FMA 1  // 1: dft<16> in FMA-form decimation in time (same contract: natural in, bit-reversed out)
+#endif
+#if SZ_DFT16_FMA
+template <>
+__device__ __forceinline__ void dft<16, false>(double2 (&x)[16]) {
+  double2 y[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) y[r] = x[bitrev4_(r)];
+  dit16_stage<false, 1>(y);
+#pragma unroll
+  for (int r = 0; r < 16; r++) x[r] = y[bitrev4_(r)];
+}
+template <>
+__device__ __forceinline__ void dft<16, true>(double2 (&x)[16]) {
+  double2 y[16];
+#pragma unroll
+  for (int r = 0; r < 16; r++) y[r] = x[bitrev4_(r)];
+  dit16_stage<true, 1>(y);
+#pragma unroll
+  for (int r = 0; r < 16; r++) x[r] = y[bitrev4_(r)];
+}
+#endif
+
 __host__ __device__ constexpr int bitrev4(int r) {
   return ((r & 1) << 3) | ((r & 2) << 1) | ((r & 4) >> 1) | ((r & 8) >> 3);
 }
