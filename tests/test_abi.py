@@ -126,3 +126,45 @@ def test_binding_rejects_malformed_tensors_before_the_call():
         silenzio.pbs_batch(ct, ok_ids, luts, None, None, P, out=torch.zeros((2, P.big_dim + 1), dtype=torch.int64))
     with pytest.raises(silenzio.SilenzioError):
         silenzio.blind_rotate_batch(ct, ok_ids, luts, None, P)   # expects n+1 words
+
+
+def test_fused_linear_pbs_and_ksk_planes_validation_without_gpu(lib):
+    """Host logic of the round-2 entry points (SURVEY §8(a) a0 fused into a1): plane and
+    workspace sizing, and the checks made before anything is launched."""
+    import torch
+    from paper_2504_17785_b200 import silenzio
+    from synth import get_params
+    L = silenzio.load()
+    PA = get_params("A")
+    P = silenzio.make_params(PA)
+    # 24 column blocks of 32 outputs x (2048 x 5) K bytes x 8 byte planes
+    assert silenzio.ksk_planes_bytes(PA) == 24 * 2048 * 5 * 256
+    assert silenzio.pbs_linear_workspace_bytes(PA, 1000) >= 1000 * 743 * 8 + 1024 * 2048 * 5
+    # set B's return keyswitch (32768 -> 2048, base 2^10): digits do not fit int8, no tensor-core planes
+    PB = get_params("B")
+    bad = silenzio.make_params(PB)
+    bad.ks_base_log = 10
+    assert L.silenzio_ksk_planes_bytes(ctypes.byref(bad)) == 0
+    fake = ctypes.c_void_p(256)
+    assert L.silenzio_ksk_to_planes(fake, fake, ctypes.byref(bad), None) == -2
+    assert L.silenzio_ksk_to_planes(None, fake, ctypes.byref(P), None) == -3
+    assert L.silenzio_ksk_to_planes(fake, ctypes.c_void_p(264), ctypes.byref(P), None) == -4   # planes: 16-byte aligned
+    args = lambda **kw: [kw.get("inp", fake), kw.get("idx", None), kw.get("coef", None), kw.get("cst", None),  # noqa: E731
+                         kw.get("terms", 1), None, fake, 1, fake, kw.get("planes", fake), fake, kw.get("count", 5),
+                         ctypes.byref(P), kw.get("ws", fake), None]
+    assert L.silenzio_pbs_linear_batch(*args(inp=None)) == -3
+    assert L.silenzio_pbs_linear_batch(*args(coef=fake)) == -1             # coefficients without indices
+    assert L.silenzio_pbs_linear_batch(*args(idx=fake, coef=None)) == -1   # indices without coefficients
+    assert L.silenzio_pbs_linear_batch(*args(idx=fake, coef=fake, terms=0)) == -1
+    assert L.silenzio_pbs_linear_batch(*args(ws=None)) == -8
+    assert L.silenzio_pbs_linear_batch(*args(count=0)) == 0
+    assert L.silenzio_pbs_linear_batch(*args(count=(1 << 31) + 1)) == -5
+    # the binding checks dtypes / shapes the raw pointers cannot show
+    ct = torch.zeros((4, PA.big_dim + 1), dtype=torch.int64)
+    luts = torch.zeros((1, PA.N), dtype=torch.int64)
+    idx = torch.zeros((3, 2), dtype=torch.int32)
+    coef = torch.ones((3, 2), dtype=torch.int64)
+    for kw in [dict(idx=idx.to(torch.int64), coef=coef), dict(idx=idx, coef=coef[:2]), dict(idx=idx, coef=None),
+               dict(idx=idx + 4, coef=coef), dict(idx=None, coef=coef)]:
+        with pytest.raises(silenzio.SilenzioError):
+            silenzio.pbs_linear_batch(ct, kw["idx"], kw["coef"], None, None, luts, None, None, PA)
