@@ -293,9 +293,15 @@ __device__ __forceinline__ void fwd_fft32(double2 (&x)[32], double2 *buf, int la
 // Inverse transform (unnormalised). In: slot order. Out: x[m] = M (c_j + i c_{j+1024}) w^{32 m},
 // j = lane + 32 m, i.e. before the final untwist conj(w^{32m}) (done by the caller:
 // untwist_round fuses it with the exact rounding; UNTWIST = true applies it here).
-template <bool UNTWIST>
-__device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, int lane) {
+struct NoHook32 {
+  __device__ __forceinline__ void operator()() const {}
+};
+// `after_pass1` runs after the first radix-32 pass (pure register arithmetic): a place for
+// work whose inputs were requested before the call (the stage-release atomic's result)
+template <bool UNTWIST, class Hook = NoHook32>
+__device__ __forceinline__ void inv_fft32(double2 (&x)[32], double2 *buf, int lane, Hook after_pass1 = Hook()) {
   dft32<true>(x);  // x[l] = 32 B'[l][k1 = lane]
+  after_pass1();
   __syncwarp();
 #pragma unroll
   for (int l = 0; l < 32; l++) buf[sw(l, lane)] = x[l];
@@ -613,12 +619,17 @@ __global__ void __launch_bounds__(Lay<SMALL>::threads, 1) blind_rotate_warp_kern
         // this warp is done with the stage; the last warp of the round re-arms it
         // with the next (i, limb) -- no CTA-wide barrier
         __syncwarp();
-        if (lane == 0 && (stage_release(&mac_done) % kW) == kW - 1) {
-          if (p > 0) issue(i, p - 1);
-          else if (i + 1 < n) issue(i + 1, P - 1);
-        }
+        // the release atomic's result (am I the last warp of the round?) is looked at only
+        // after the inverse transform's first pass, so its latency hides behind that pass
+        uint32_t rel = 0;
+        if (lane == 0) rel = stage_release(&mac_done);
         constexpr bool kFusedUntwist = (P == 3);
-        inv_fft32<!kFusedUntwist>(y, xbuf, lane);
+        inv_fft32<!kFusedUntwist>(y, xbuf, lane, [&]() {
+          if (lane == 0 && (rel % kW) == kW - 1) {
+            if (p > 0) issue(i, p - 1);
+            else if (i + 1 < n) issue(i + 1, P - 1);
+          }
+        });
         SZ_PT(6);
         // P = 3: bits(x + 1.5 2^52) << 22p per limb, the magic constant's share of
         // all three limbs removed once per CMux (at p = 0)
